@@ -925,7 +925,7 @@ def assemble(cfg, kvs, storage="f32"):
         pos = np.arange(cursor, cursor + n)
         for l in range(L):
             ks[l].append(rnd(rotate(kv["k"][l], pos, cfg, cfg.kv_heads)))
-            vs[l].append(kv["v"][l])
+            vs[l].append(rnd(kv["v"][l]) if storage == "bf16" else kv["v"][l])  # bf16 prefix slab
         spans.append((cursor, cursor + n))
         cursor += n
     ks = [np.concatenate(k) if k else np.zeros((0, cfg.kv_dim)) for k in ks]

@@ -1,0 +1,126 @@
+// Prefix assembly: the device form of assemble() (proj/include/tablekv/attention.hpp:300-362).
+//
+// One warp per output token row. The warp finds its table segment (binary search over the
+// contiguous output ranges), then for each layer and for K and V reads the row out of the
+// table's pool pages with 16-byte vector loads, rotates K at the token's global position
+// (cursor + t, interleaved pairs, rotary.hpp:21-51) and writes the row into the per-layer
+// prefix slab. HBM-bound: algorithmic bytes = rows * 2L * kvdim * (in + out element size).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tkv {
+
+namespace {
+
+template <int EPV>
+struct Vec;  // EPV elements held as float
+template <>
+struct Vec<4> { float v[4]; };
+template <>
+struct Vec<8> { float v[8]; };
+
+__device__ __forceinline__ void load_in(const uint8_t* p, DType dt, float* f, int& n) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(p);
+    if (dt == DType::f32) {
+        f[0] = __uint_as_float(raw.x);
+        f[1] = __uint_as_float(raw.y);
+        f[2] = __uint_as_float(raw.z);
+        f[3] = __uint_as_float(raw.w);
+        n = 4;
+    } else {
+        float2 a = unpack_bf16x2(raw.x), b = unpack_bf16x2(raw.y), c = unpack_bf16x2(raw.z), d = unpack_bf16x2(raw.w);
+        f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y; f[4] = c.x; f[5] = c.y; f[6] = d.x; f[7] = d.y;
+        n = 8;
+    }
+}
+
+__device__ __forceinline__ void store_out(uint8_t* p, DType dt, const float* f, int n) {
+    if (dt == DType::f32) {
+        for (int i = 0; i < n; i += 4)
+            *reinterpret_cast<uint4*>(p + i * 4) =
+                make_uint4(__float_as_uint(f[i]), __float_as_uint(f[i + 1]), __float_as_uint(f[i + 2]), __float_as_uint(f[i + 3]));
+    } else if (n == 8) {
+        *reinterpret_cast<uint4*>(p) =
+            make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+    } else {
+        *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]));
+    }
+}
+
+__global__ void gather_rope_kernel(const uint8_t* __restrict__ pool, long page_bytes, const int32_t* __restrict__ page_ids,
+                                   const GatherSeg* __restrict__ segs, int n_segs, int total_rows, int L, int kvdim,
+                                   int head_dim, DType in_dt, DType out_dt, const double* __restrict__ cos_d,
+                                   const double* __restrict__ sin_d, const float* __restrict__ cos_f,
+                                   const float* __restrict__ sin_f, uint8_t* __restrict__ out_k,
+                                   uint8_t* __restrict__ out_v, long out_rows) {
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= total_rows) return;
+    int lo = 0, hi = n_segs - 1;
+    while (lo < hi) {  // last segment with out_row0 <= row
+        const int mid = (lo + hi + 1) >> 1;
+        if (segs[mid].out_row0 <= row) lo = mid; else hi = mid - 1;
+    }
+    const GatherSeg sg = segs[lo];
+    const int t = row - sg.out_row0;
+    const long pos = sg.pos0 + t;
+    const int half = head_dim >> 1;
+    const int isz = in_dt == DType::f32 ? 4 : 2, osz = out_dt == DType::f32 ? 4 : 2;
+    const int epv = 16 / isz;  // elements per input vector
+    const long row_in = long(kvdim) * isz;
+    const int nvec = int(row_in / 16);
+    const bool exact = (in_dt == DType::f32 && out_dt == DType::f32 && cos_d != nullptr);
+    for (int kv = 0; kv < 2; ++kv) {
+        uint8_t* out = kv == 0 ? out_k : out_v;
+        for (int l = 0; l < L; ++l) {
+            const long base = ((long(kv) * L + l) * sg.tokens + t) * row_in;
+            uint8_t* orow = out + ((long(l) * out_rows) + row) * long(kvdim) * osz;
+            for (int vi = lane; vi < nvec; vi += 32) {
+                const long off = base + long(vi) * 16;
+                const long pg = off / page_bytes;
+                const uint8_t* src = pool + long(page_ids[sg.page_off + pg]) * page_bytes + (off - pg * page_bytes);
+                float f[8];
+                int n;
+                load_in(src, in_dt, f, n);
+                const int e0 = vi * epv;
+                if (kv == 0 && pos != 0) {
+                    for (int i = 0; i < n; i += 2) {
+                        const int k = ((e0 + i) % head_dim) >> 1;
+                        if (exact) {
+                            // a*c - b*s, a*s + b*c in double, each product rounded (no FMA contraction),
+                            // exactly like the reference's double arithmetic (rotary.hpp:44-47)
+                            const double c = cos_d[pos * half + k], s = sin_d[pos * half + k];
+                            const double a = f[i], b = f[i + 1];
+                            f[i] = float(__dsub_rn(__dmul_rn(a, c), __dmul_rn(b, s)));
+                            f[i + 1] = float(__dadd_rn(__dmul_rn(a, s), __dmul_rn(b, c)));
+                        } else {
+                            const float c = cos_f[pos * half + k], s = sin_f[pos * half + k];
+                            const float a = f[i], b = f[i + 1];
+                            f[i] = fmaf(a, c, -b * s);
+                            f[i + 1] = fmaf(a, s, b * c);
+                        }
+                    }
+                }
+                store_out(orow + long(e0) * osz, out_dt, f, n);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
+                        int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,
+                        const double* cos_d, const double* sin_d, const float* cos_f, const float* sin_f, void* out_k,
+                        void* out_v, long out_rows, cudaStream_t s) {
+    if (total_rows <= 0 || n_segs <= 0) return;
+    if ((long(kvdim) * dtype_size(in_dt)) % 16) throw std::invalid_argument("gather: kv row must be a multiple of 16 bytes");
+    const int warps = 8;
+    gather_rope_kernel<<<ceil_div(total_rows, warps), warps * 32, 0, s>>>(
+        pool, long(page_bytes), d_page_ids, d_segs, n_segs, total_rows, L, kvdim, head_dim, in_dt, out_dt, cos_d, sin_d,
+        cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v), out_rows);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tkv

@@ -1,0 +1,349 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a with fused epilogues (the QKV/O/MLP/head projections
+// of query_attend, proj/include/tablekv/attention.hpp:387-411, as dense tensor-core work).
+//
+// CTA tile 128 x BN x 64 (bf16, 128-byte swizzle), STAGES-deep TMA->smem ring guarded by
+// mbarriers, one elected thread issues tcgen05.mma (M=128, N=BN, K=16) into a TMEM f32
+// accumulator, tcgen05.commit releases smem slots and finally signals the epilogue; all four
+// warps then drain TMEM (tcgen05.ld 32x32b, one accumulator row per thread) through the fused
+// epilogue (RoPE / SiLU / SwiGLU / residual add) straight to global memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace tkv {
+
+namespace {
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit accumulators: thread i gets row (lane base + i), 32 columns.
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: rows 128 B apart, 8-row groups
+// 1024 B apart (SBO), LBO unused (=1), version 1 (sm100), layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return uint64_t((saddr & 0x3FFFF) >> 4) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) | (uint64_t(1) << 46) |
+           (uint64_t(2) << 61);
+}
+
+// Instruction descriptor: D f32, A/B bf16, both K-major, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ fused epilogue
+// v[0..31] = accumulator row m, columns n0..n0+31 (n0 % 32 == 0).
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        d[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                          pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+}
+
+__device__ __forceinline__ void rope32(float* v, int col0, int head_dim, int pos, const float* cos_f, const float* sin_f) {
+    const int half = head_dim >> 1;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+        const int k = ((col0 + i) % head_dim) >> 1;
+        const float c = cos_f[long(pos) * half + k], s = sin_f[long(pos) * half + k];
+        const float a = v[i], b = v[i + 1];
+        v[i] = fmaf(a, c, -b * s);
+        v[i + 1] = fmaf(a, s, b * c);
+    }
+}
+
+__device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
+
+__device__ void epilogue32(const EpiParams& ep, int m, int n0, float* v) {
+    switch (ep.kind) {
+        case Epi::store_bf16:
+            store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + long(m) * ep.ldo + n0, v);
+            break;
+        case Epi::store_f32: {
+            float4* d = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + long(m) * ep.ldo + n0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            break;
+        }
+        case Epi::resid_f32: {
+            float4* d = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + long(m) * ep.ldo + n0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float4 r = d[i];
+                r.x += v[4 * i], r.y += v[4 * i + 1], r.z += v[4 * i + 2], r.w += v[4 * i + 3];
+                d[i] = r;
+            }
+            break;
+        }
+        case Epi::silu_bf16:
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = silu_f(v[i]);
+            store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + long(m) * ep.ldo + n0, v);
+            break;
+        case Epi::swiglu_bf16: {
+            float o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = silu_f(v[i]) * v[16 + i];
+            uint4* d = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + long(m) * ep.ldo + n0 / 2);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                d[i] = make_uint4(pack_bf16x2(o[8 * i], o[8 * i + 1]), pack_bf16x2(o[8 * i + 2], o[8 * i + 3]),
+                                  pack_bf16x2(o[8 * i + 4], o[8 * i + 5]), pack_bf16x2(o[8 * i + 6], o[8 * i + 7]));
+            break;
+        }
+        case Epi::qkv_rope: {
+            const int pos = ep.pos[m];
+            if (n0 < ep.q_cols) {
+                rope32(v, n0, ep.head_dim, pos, ep.cos_f, ep.sin_f);
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.q_out) + long(m) * ep.q_cols + n0, v);
+            } else if (n0 < ep.q_cols + ep.kv_cols) {
+                const int c = n0 - ep.q_cols;
+                if (ep.k_raw_out) store_bf16x32(static_cast<__nv_bfloat16*>(ep.k_raw_out) + long(m) * ep.kv_cols + c, v);
+                rope32(v, c, ep.head_dim, pos, ep.cos_f, ep.sin_f);
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.k_out) + long(m) * ep.kv_cols + c, v);
+            } else {
+                const int c = n0 - ep.q_cols - ep.kv_cols;
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.v_out) + long(m) * ep.kv_cols + c, v);
+            }
+            break;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ the kernel
+constexpr int BM = 128, BK = 64;
+
+template <int BN, int STAGES>
+struct Smem {
+    static constexpr int a_bytes = BM * BK * 2;
+    static constexpr int b_bytes = BN * BK * 2;
+    static constexpr int stage_bytes = a_bytes + b_bytes;
+    static constexpr int bars_off = STAGES * stage_bytes;
+    static constexpr int total = bars_off + (2 * STAGES + 1) * 8 + 16 + 1024;  // + alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                   const __grid_constant__ EpiParams ep) {
+    using S = Smem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), done = smem_u32(bars + 2 * STAGES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 2) {  // TMEM: BN f32 columns x 128 lanes
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer
+        for (int kb = 0; kb < nk; ++kb) {
+            const int st = kb % STAGES;
+            mbar_wait(empty0 + 8 * st, ((kb / STAGES) & 1) ^ 1);
+            const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+            mbar_expect_tx(full0 + 8 * st, S::stage_bytes);
+            tma_load_2d(sa, &tmA, full0 + 8 * st, kb * BK, m0);
+            tma_load_2d(sa + S::a_bytes, &tmB, full0 + 8 * st, kb * BK, n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer
+        constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+        for (int kb = 0; kb < nk; ++kb) {
+            const int st = kb % STAGES;
+            mbar_wait(full0 + 8 * st, (kb / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+            const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + S::a_bytes);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
+                tc_mma(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            tc_commit(empty0 + 8 * st);
+        }
+        tc_commit(done);
+    }
+    __syncwarp();
+
+    // ---- epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int m = m0 + warp * 32 + lane;
+    for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c, v);
+        if (m < M && n0 + c < N) epilogue32(ep, m, n0 + c, v);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+}
+
+// ------------------------------------------------------------------ SIMT reference
+__global__ void gemm_simt_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B, int M, int N,
+                                 int K, EpiParams ep) {
+    const long idx = blockIdx.x * long(blockDim.x) + threadIdx.x;
+    const int chunks = N / 32;
+    if (idx >= long(M) * chunks) return;
+    const int m = int(idx / chunks), n0 = int(idx % chunks) * 32;
+    float v[32];
+    for (int j = 0; j < 32; ++j) {
+        float acc = 0.f;
+        for (int k = 0; k < K; ++k)
+            acc = fmaf(__bfloat162float(A[long(m) * K + k]), __bfloat162float(B[long(n0 + j) * K + k]), acc);
+        v[j] = acc;
+    }
+    epilogue32(ep, m, n0, v);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        TKV_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+CUtensorMap make_map_2d(const void* base, int rows, int cols, int box_rows) {
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+    const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return map;
+}
+
+template <int BN, int STAGES>
+void launch_tc(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    using S = Smem<BN, STAGES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::total));
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map_2d(A, M, K, BM);
+    const CUtensorMap tb = make_map_2d(B, N, K, BN);
+    dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+    gemm_tc_kernel<BN, STAGES><<<grid, 128, S::total, s>>>(ta, tb, M, N, K, ep);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace
+
+void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    if (M == 0) return;
+    if (K % 8 || N % 32) throw std::invalid_argument("gemm_bf16: need K % 8 == 0 and N % 32 == 0");
+    // Wide N with enough rows: 128x256 tiles (one CTA per SM, 4 stages); otherwise 128x128
+    // tiles at 2 CTAs per SM so one CTA's epilogue overlaps the other's main loop.
+    const long tiles256 = long((N + 255) / 256) * ((M + BM - 1) / BM);
+    if (N % 256 == 0 && tiles256 >= 2 * kNumSMs)
+        launch_tc<256, 4>(A, B, M, N, K, ep, s);
+    else
+        launch_tc<128, 3>(A, B, M, N, K, ep, s);
+}
+
+void gemm_bf16_simt(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    if (M == 0) return;
+    const long n = long(M) * (N / 32);
+    gemm_simt_kernel<<<ceil_div(n, 128), 128, 0, s>>>(static_cast<const __nv_bfloat16*>(A),
+                                                      static_cast<const __nv_bfloat16*>(B), M, N, K, ep);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tkv

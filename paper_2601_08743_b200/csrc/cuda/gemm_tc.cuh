@@ -1,0 +1,41 @@
+// bf16 x bf16 -> f32 tcgen05 GEMM with fused epilogues: C[M][N] = A[M][K] . B[N][K]^T.
+// A = activations (row-major, K contiguous), B = weights in the reference's row-major
+// [out][in] layout (model.hpp:49-51), so both operands are K-major for UMMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tkv {
+
+enum class Epi : int {
+    store_bf16 = 0,   // out_bf16[m][n]
+    store_f32 = 1,    // out_f32[m][n]
+    resid_f32 = 2,    // resid[m][n] += acc          (O-proj / down-proj, residual stream)
+    silu_bf16 = 3,    // out_bf16[m][n] = silu(acc)  (reference non-gated MLP)
+    swiglu_bf16 = 4,  // 16-col interleaved [gate|up]: out[m][n/2] = silu(g) * u
+    qkv_rope = 5,     // split q | k | v, interleaved RoPE on q, k at pos[m]
+};
+
+struct EpiParams {
+    Epi kind = Epi::store_bf16;
+    void* out = nullptr;        // bf16/f32 output or residual (f32)
+    long ldo = 0;               // output row stride (elements)
+    // qkv_rope
+    void* q_out = nullptr;      // [M][q_cols] bf16
+    void* k_out = nullptr;      // [M][kv_cols] bf16 (rotated)
+    void* k_raw_out = nullptr;  // optional [M][kv_cols] bf16 pre-rotation (offline encode keeps it)
+    void* v_out = nullptr;      // [M][kv_cols] bf16
+    int q_cols = 0, kv_cols = 0, head_dim = 0;
+    const int32_t* pos = nullptr;        // [M] global positions
+    const float* cos_f = nullptr;        // [max_pos][head_dim/2]
+    const float* sin_f = nullptr;
+};
+
+// Launch on stream; A, B device pointers (bf16 bits), K % 8 == 0, N % 32 == 0.
+void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);
+
+// Simple SIMT bf16 GEMM with the same epilogues (correctness reference for tests only).
+void gemm_bf16_simt(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);
+
+}  // namespace tkv

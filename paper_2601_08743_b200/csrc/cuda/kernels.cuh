@@ -1,0 +1,77 @@
+// Launchers for every device kernel of the online path (host-callable, stream-ordered).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tkv {
+
+enum class DType : int { f32 = 0, bf16 = 1, f64 = 2 };
+
+inline size_t dtype_size(DType d) { return d == DType::bf16 ? 2 : (d == DType::f32 ? 4 : 8); }
+
+// ---- init.cu: weight init from the counter hash (proj/include/tablekv/model.hpp:80-87) -----
+// dst row (interleaved) <- source row r of a [rows x cols] matrix whose element i is
+// float(signed_unit(mix3(seed, tag_stream, i)) * scale). interleave_block == 0 means rows
+// land contiguously at dst_row0 + r; otherwise source row r lands at
+// (r / ib) * 2ib + slot * ib + r % ib (SwiGLU gate/up interleave for the fused epilogue).
+void launch_fill_matrix(void* dst, DType dt, long rows, long cols, long dst_row0, uint64_t seed, uint64_t tag_stream,
+                        double scale, int interleave_block, int slot, cudaStream_t s);
+
+// ---- kvload.cu: slow tier -> paged HBM pool ------------------------------------------------
+constexpr int kMaxPagesPerCopy = 256;
+struct PageList {
+    int32_t n;
+    int32_t page[kMaxPagesPerCopy];
+};
+// SM-driven copy of a table image from mapped pinned host memory into its pool pages with
+// coalesced 16-byte loads/stores (the north-star "vectorised H2D"); bytes % 16 == 0.
+void launch_h2d_pages(const void* src_mapped, size_t bytes, uint8_t* pool, size_t page_bytes, const PageList& pages,
+                      int n_ctas, cudaStream_t s);
+// Device-to-device variant (peer pool pointer or local), same page addressing on both sides.
+void launch_d2d_pages(const uint8_t* src_pool, size_t src_page_bytes, const PageList& src_pages, uint8_t* dst_pool,
+                      size_t dst_page_bytes, const PageList& dst_pages, size_t bytes, cudaStream_t s);
+
+// ---- gather.cu: assemble (proj/include/tablekv/attention.hpp:300-362) ----------------------
+struct GatherSeg {
+    int32_t page_off;  // index of the table's first page id in the page-id array
+    int32_t tokens;    // table token count T
+    int32_t pos0;      // global position of the table's first token (cursor)
+    int32_t out_row0;  // first output row (segments are contiguous in output rows)
+};
+// Out layout: out_k / out_v are [L][out_rows][kvdim]; the table image in the pool is the
+// .kv layout [K: L][T][kvdim] then [V: L][T][kvdim] (table_kv.hpp:45-48) addressed through
+// its pages. K is rotated at pos0 + t (interleaved pairs); V is copied.
+// exact (f32 in/out): cos/sin double tables, double arithmetic without contraction =>
+// bit-identical to the reference's rotated_copy. fast: f32 math, any in/out dtype.
+void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
+                        int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,
+                        const double* cos_d, const double* sin_d, const float* cos_f, const float* sin_f,
+                        void* out_k, void* out_v, long out_rows, cudaStream_t s);
+
+// ---- rope tables ------------------------------------------------------------------------------
+// Host-built [max_pos][head_dim/2] tables: angle = pos * pow(base, -2k/d) in double, std::cos /
+// std::sin (rotary.hpp:31-39), so device rotation uses the reference's exact factors.
+
+// ---- simt.cu: reference-precision (double-accumulate) forward pieces, any T in {float,double} --
+void launch_embed(const void* emb, DType dt, const int32_t* tokens, int n, int hidden, void* x, cudaStream_t s);
+void launch_layer_norm_ref(const void* x, void* out, DType dt, int rows, int hidden, int rms, double eps, cudaStream_t s);
+void launch_matmul_ref(const void* w, const void* x, void* y, DType dt, int rows_out, int cols_in, int tokens,
+                       int act_silu, cudaStream_t s);
+void launch_add_ref(void* x, const void* y, DType dt, long n, cudaStream_t s);
+void launch_mul_ref(void* x, const void* y, DType dt, long n, cudaStream_t s);
+void launch_rope_ref(void* x, DType dt, const int64_t* positions, int n, int heads, int head_dim,
+                     const double* cos_d, const double* sin_d, int table_pos, cudaStream_t s);
+// attention over [ctx ; own] per sequence; mask mode 0: own rows see all ctx + causal own,
+// mode 1: block-causal by group id (BlockMask::allows, attention.hpp:37-39), no ctx.
+struct AttnSeq {
+    int32_t q_row0;    // first own row in q / own k / own v (token rows)
+    int32_t n_own;
+    int32_t ctx_row0;  // first ctx row in ctx k / v
+    int32_t n_ctx;
+};
+void launch_attend_ref(const void* q, const void* k_own, const void* v_own, const void* k_ctx, const void* v_ctx,
+                       const int32_t* group, const AttnSeq* seqs, int n_seqs, int total_q, void* out, DType dt,
+                       int num_heads, int kv_heads, int head_dim, int mode, cudaStream_t s);
+
+}  // namespace tkv

@@ -1,0 +1,419 @@
+// Device model: weight init + the prefill forward in two precisions.
+//   bf16 (performance path): tcgen05 GEMMs with fused RoPE / SiLU|SwiGLU / residual epilogues,
+//     tensor-core attention over [cached prefix ; own rows], f32 residual stream.
+//   f32 / f64 (reference-precision path): the SIMT kernels of simt.cu, operation-for-operation
+//     the reference's arithmetic (attention.hpp:210-247 and :368-414).
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "model.cuh"
+#include "norm.cuh"
+
+namespace tkv {
+
+// ------------------------------------------------------------------ StagingRing
+StagingRing::StagingRing(size_t bytes) : cap_(bytes) {
+    TKV_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), bytes, cudaHostAllocDefault));
+    TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&dev_), bytes));
+}
+
+StagingRing::~StagingRing() {
+    cudaFreeHost(host_);
+    cudaFree(dev_);
+}
+
+void* StagingRing::upload(const void* src, size_t n, cudaStream_t s) {
+    n = (n + 255) & ~size_t(255);
+    if (n > cap_) throw std::runtime_error("staging ring too small for one upload");
+    if (off_ + n > cap_) {
+        // wrap: every earlier chunk may still be read by queued work
+        TKV_CUDA_CHECK(cudaDeviceSynchronize());
+        off_ = 0;
+    }
+    std::memcpy(host_ + off_, src, n);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(dev_ + off_, host_ + off_, n, cudaMemcpyHostToDevice, s));
+    void* d = dev_ + off_;
+    off_ += n;
+    return d;
+}
+
+// ------------------------------------------------------------------ RopeTables
+RopeTables::RopeTables(int head_dim, double base) : d_(head_dim), base_(base) {}
+
+RopeTables::~RopeTables() {
+    cudaFree(cos_d_);
+    cudaFree(sin_d_);
+    cudaFree(cos_f_);
+    cudaFree(sin_f_);
+}
+
+void RopeTables::ensure(int max_pos) {
+    if (max_pos <= max_pos_) return;
+    int cap = std::max(4096, max_pos_);
+    while (cap < max_pos) cap *= 2;
+    TKV_CUDA_CHECK(cudaDeviceSynchronize());
+    cudaFree(cos_d_);
+    cudaFree(sin_d_);
+    cudaFree(cos_f_);
+    cudaFree(sin_f_);
+    const int half = d_ / 2;
+    std::vector<double> inv(half), cd(size_t(cap) * half), sd(size_t(cap) * half);
+    std::vector<float> cf(cd.size()), sf(cd.size());
+    for (int k = 0; k < half; ++k) inv[k] = std::pow(base_, -2.0 * k / d_);
+    for (long p = 0; p < cap; ++p)
+        for (int k = 0; k < half; ++k) {
+            const double angle = double(p) * inv[k];
+            cd[p * half + k] = std::cos(angle);
+            sd[p * half + k] = std::sin(angle);
+            cf[p * half + k] = float(cd[p * half + k]);
+            sf[p * half + k] = float(sd[p * half + k]);
+        }
+    TKV_CUDA_CHECK(cudaMalloc(&cos_d_, cd.size() * 8));
+    TKV_CUDA_CHECK(cudaMalloc(&sin_d_, cd.size() * 8));
+    TKV_CUDA_CHECK(cudaMalloc(&cos_f_, cd.size() * 4));
+    TKV_CUDA_CHECK(cudaMalloc(&sin_f_, cd.size() * 4));
+    TKV_CUDA_CHECK(cudaMemcpy(cos_d_, cd.data(), cd.size() * 8, cudaMemcpyHostToDevice));
+    TKV_CUDA_CHECK(cudaMemcpy(sin_d_, sd.data(), sd.size() * 8, cudaMemcpyHostToDevice));
+    TKV_CUDA_CHECK(cudaMemcpy(cos_f_, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
+    TKV_CUDA_CHECK(cudaMemcpy(sin_f_, sf.data(), sf.size() * 4, cudaMemcpyHostToDevice));
+    max_pos_ = cap;
+}
+
+// ------------------------------------------------------------------ Model
+namespace {
+// weight tags (model.hpp:36-44) + extensions: 8 = untied LM head, 9 = SwiGLU gate
+constexpr uint64_t kEmb = 1, kWq = 2, kWk = 3, kWv = 4, kWo = 5, kIn = 6, kOut = 7, kHead = 8, kGate = 9;
+}  // namespace
+
+Model::Model(const ModelCfg& cfg, cudaStream_t s) : cfg_(cfg), rope_(cfg.head_dim, cfg.rotary_base), ring_(64u << 20) {
+    if (cfg.num_heads % cfg.kv_heads) throw std::invalid_argument("num_heads must be a multiple of kv_heads");
+    if (cfg.head_dim % 2) throw std::invalid_argument("head_dim must be even for rotary pairs");
+    if (cfg.vocab <= 0) throw std::invalid_argument("vocab must be positive");
+    alloc_weights(s);
+    rope_.ensure(8192);
+}
+
+Model::~Model() {
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    for (void* p : allocs_) cudaFree(p);
+    cudaFree(ws_);
+}
+
+void Model::alloc_weights(cudaStream_t s) {
+    const ModelCfg& c = cfg_;
+    const long h = c.hidden(), kvd = c.kv_dim(), f = c.ffn, qd = long(c.num_heads) * c.head_dim;
+    const size_t es = dtype_size(c.dtype);
+    auto alloc = [&](long elems) {
+        void* p = nullptr;
+        TKV_CUDA_CHECK(cudaMalloc(&p, size_t(elems) * es));
+        allocs_.push_back(p);
+        weight_bytes_ += size_t(elems) * es;
+        return p;
+    };
+    const double sh = 1.0 / std::sqrt(double(h)), sf = 1.0 / std::sqrt(double(f));
+    emb_ = alloc(long(c.vocab) * h);
+    launch_fill_matrix(emb_, c.dtype, c.vocab, h, 0, c.seed, kEmb * 131, 0.5, 0, 0, s);
+    layers_.resize(c.num_layers);
+    for (int l = 0; l < c.num_layers; ++l) {
+        Layer& L = layers_[l];
+        if (c.dtype == DType::bf16) {
+            L.wqkv = alloc((qd + 2 * kvd) * h);
+            launch_fill_matrix(L.wqkv, c.dtype, qd, h, 0, c.seed, kWq * 131 + l, sh, 0, 0, s);
+            launch_fill_matrix(L.wqkv, c.dtype, kvd, h, qd, c.seed, kWk * 131 + l, sh, 0, 0, s);
+            launch_fill_matrix(L.wqkv, c.dtype, kvd, h, qd + kvd, c.seed, kWv * 131 + l, sh, 0, 0, s);
+            if (c.mlp == 1) {  // [gate 16 | up 16] row blocks for the fused SwiGLU epilogue
+                L.w_in = alloc(2 * f * h);
+                launch_fill_matrix(L.w_in, c.dtype, f, h, 0, c.seed, kGate * 131 + l, sh, 16, 0, s);
+                launch_fill_matrix(L.w_in, c.dtype, f, h, 0, c.seed, kIn * 131 + l, sh, 16, 1, s);
+            } else {
+                L.w_in = alloc(f * h);
+                launch_fill_matrix(L.w_in, c.dtype, f, h, 0, c.seed, kIn * 131 + l, sh, 0, 0, s);
+            }
+        } else {
+            L.wq = alloc(qd * h);
+            L.wk = alloc(kvd * h);
+            L.wv = alloc(kvd * h);
+            launch_fill_matrix(L.wq, c.dtype, qd, h, 0, c.seed, kWq * 131 + l, sh, 0, 0, s);
+            launch_fill_matrix(L.wk, c.dtype, kvd, h, 0, c.seed, kWk * 131 + l, sh, 0, 0, s);
+            launch_fill_matrix(L.wv, c.dtype, kvd, h, 0, c.seed, kWv * 131 + l, sh, 0, 0, s);
+            L.w_in = alloc(f * h);
+            launch_fill_matrix(L.w_in, c.dtype, f, h, 0, c.seed, kIn * 131 + l, sh, 0, 0, s);
+            if (c.mlp == 1) {
+                L.w_gate = alloc(f * h);
+                launch_fill_matrix(L.w_gate, c.dtype, f, h, 0, c.seed, kGate * 131 + l, sh, 0, 0, s);
+            }
+        }
+        L.wo = alloc(h * qd);
+        launch_fill_matrix(L.wo, c.dtype, h, qd, 0, c.seed, kWo * 131 + l, sh, 0, 0, s);
+        L.w_out = alloc(h * f);
+        launch_fill_matrix(L.w_out, c.dtype, h, f, 0, c.seed, kOut * 131 + l, sf, 0, 0, s);
+    }
+    const long vp = c.dtype == DType::bf16 ? c.vocab_padded() : c.vocab;
+    head_ = alloc(vp * h);
+    TKV_CUDA_CHECK(cudaMemsetAsync(head_, 0, size_t(vp * h) * es, s));
+    launch_fill_matrix(head_, c.dtype, c.vocab, h, 0, c.seed, kHead * 131, sh, 0, 0, s);
+    TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void Model::ensure_ws(int M, cudaStream_t s) {
+    if (M <= ws_rows_) return;
+    int cap = std::max(256, ws_rows_);
+    while (cap < M) cap *= 2;
+    TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(ws_);
+    const ModelCfg& c = cfg_;
+    const size_t es = dtype_size(c.dtype);
+    const long h = c.hidden(), qd = long(c.num_heads) * c.head_dim, kvd = c.kv_dim(), f = c.ffn;
+    // x (f32 or T), xn, q, k, v, attn, proj (T), mid (f), gate (f)
+    const size_t per_row = size_t(h) * std::max<size_t>(4, es) + (h + qd + 2 * kvd + qd + h) * es + 2 * size_t(f) * es + 64;
+    TKV_CUDA_CHECK(cudaMalloc(&ws_, per_row * cap + 4096));
+    ws_rows_ = cap;
+}
+
+void Model::forward(const FwdArgs& a, cudaStream_t s) {
+    if (a.M == 0) return;
+    ensure_ws(a.M, s);
+    if (cfg_.dtype == DType::bf16)
+        forward_bf16(a, s);
+    else
+        forward_ref(a, s);
+}
+
+cudaEvent_t Model::timing_event() {
+    if (ev_used_ == ev_pool_.size()) {
+        cudaEvent_t e;
+        TKV_CUDA_CHECK(cudaEventCreate(&e));
+        ev_pool_.push_back(e);
+    }
+    return ev_pool_[ev_used_++];
+}
+
+void Model::add_timed(cudaEvent_t a, cudaEvent_t b, double flops) {
+    timed_.push_back({a, b, flops < 0 ? 0.0 : flops, flops < 0 ? 2 : (flops == 0 ? 1 : 0)});
+}
+
+void Model::collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms) {
+    gemm_ms = gemm_flops = gather_ms = attn_ms = 0;
+    for (const TimedRec& r : timed_) {
+        float ms = 0;
+        TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+        if (r.kind == 0) gemm_ms += ms, gemm_flops += r.flops;
+        else if (r.kind == 1) attn_ms += ms;
+        else gather_ms += ms;
+    }
+    timed_.clear();
+    ev_used_ = 0;
+}
+
+void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
+    const ModelCfg& c = cfg_;
+    const int M = a.M, h = c.hidden(), qd = c.num_heads * c.head_dim, kvd = c.kv_dim(), f = c.ffn;
+    const int rms = c.norm == 1;
+    const float eps = float(c.eps);
+    uint8_t* p = static_cast<uint8_t*>(ws_);
+    auto take = [&](size_t bytes) {
+        void* r = p;
+        p += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    const long R = ws_rows_;
+    float* x = static_cast<float*>(take(size_t(R) * h * 4));
+    void* xn = take(size_t(R) * h * 2);
+    void* q = take(size_t(R) * qd * 2);
+    void* k = take(size_t(R) * kvd * 2);
+    void* v = take(size_t(R) * kvd * 2);
+    void* att = take(size_t(R) * qd * 2);
+    void* mid = take(size_t(R) * f * 2);
+
+    // attention work list: (seq, first token, kv head)
+    const int tq = attn_rows_per_tile(c.num_heads, c.kv_heads);
+    std::vector<int4> tiles;
+    for (int si = 0; si < a.n_seqs; ++si)
+        for (int t0 = 0; t0 < a.seqs_host[si].n_own; t0 += tq)
+            for (int kh = 0; kh < c.kv_heads; ++kh) tiles.push_back(make_int4(si, t0, kh, 0));
+    const int4* d_tiles = tiles.empty() ? nullptr
+                                        : static_cast<const int4*>(ring_.upload(tiles.data(), tiles.size() * sizeof(int4), s));
+    long nl = 0;
+    auto run_gemm = [&](const void* A, const void* B, int m, int n, int k, const EpiParams& e) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timing_) {
+            e0 = timing_event();
+            e1 = timing_event();
+            TKV_CUDA_CHECK(cudaEventRecord(e0, s));
+        }
+        gemm_bf16(A, B, m, n, k, e, s);
+        if (timing_) {
+            TKV_CUDA_CHECK(cudaEventRecord(e1, s));
+            add_timed(e0, e1, 2.0 * m * n * double(k));
+        }
+    };
+
+    embed_norm_bf16(emb_, a.tokens, M, h, x, xn, rms, eps, s);
+    ++nl;
+    for (int l = 0; l < c.num_layers; ++l) {
+        const Layer& L = layers_[l];
+        void* v_l = a.v_out ? static_cast<uint8_t*>(a.v_out) + size_t(l) * M * kvd * 2 : v;
+        EpiParams e;
+        e.kind = Epi::qkv_rope;
+        e.q_out = q;
+        e.k_out = k;
+        e.v_out = v_l;
+        e.k_raw_out = a.kraw_out ? static_cast<uint8_t*>(a.kraw_out) + size_t(l) * M * kvd * 2 : nullptr;
+        e.q_cols = qd;
+        e.kv_cols = kvd;
+        e.head_dim = c.head_dim;
+        e.pos = a.pos;
+        e.cos_f = rope_.cos_f();
+        e.sin_f = rope_.sin_f();
+        run_gemm(xn, L.wqkv, M, qd + 2 * kvd, h, e);
+
+        AttnArgs aa;
+        aa.q = static_cast<const __nv_bfloat16*>(q);
+        aa.k_own = static_cast<const __nv_bfloat16*>(k);
+        aa.v_own = static_cast<const __nv_bfloat16*>(v_l);
+        const size_t ctx_off = size_t(l) * a.ctx_rows * kvd * 2;
+        aa.k_ctx = a.ctx_k ? reinterpret_cast<const __nv_bfloat16*>(static_cast<const uint8_t*>(a.ctx_k) + ctx_off) : aa.k_own;
+        aa.v_ctx = a.ctx_v ? reinterpret_cast<const __nv_bfloat16*>(static_cast<const uint8_t*>(a.ctx_v) + ctx_off) : aa.v_own;
+        aa.group = a.group;
+        aa.seqs = a.seqs;
+        aa.tiles = d_tiles;
+        aa.out = static_cast<__nv_bfloat16*>(att);
+        aa.num_heads = c.num_heads;
+        aa.kv_heads = c.kv_heads;
+        aa.head_dim = c.head_dim;
+        aa.mode = a.mode;
+        aa.scale = float(1.0 / std::sqrt(double(c.head_dim)));
+        {
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (timing_) {
+                e0 = timing_event();
+                e1 = timing_event();
+                TKV_CUDA_CHECK(cudaEventRecord(e0, s));
+            }
+            attention_bf16(aa, int(tiles.size()), s);
+            if (timing_) {
+                TKV_CUDA_CHECK(cudaEventRecord(e1, s));
+                add_timed(e0, e1, 0.0);
+            }
+        }
+
+        EpiParams eo;
+        eo.kind = Epi::resid_f32;
+        eo.out = x;
+        eo.ldo = h;
+        run_gemm(att, L.wo, M, h, qd, eo);
+        norm_bf16(x, nullptr, M, h, xn, rms, eps, s);
+
+        EpiParams em;
+        em.out = mid;
+        em.ldo = f;
+        if (c.mlp == 1) {
+            em.kind = Epi::swiglu_bf16;
+            run_gemm(xn, L.w_in, M, 2 * f, h, em);
+        } else {
+            em.kind = Epi::silu_bf16;
+            run_gemm(xn, L.w_in, M, f, h, em);
+        }
+        EpiParams ed;
+        ed.kind = Epi::resid_f32;
+        ed.out = x;
+        ed.ldo = h;
+        run_gemm(mid, L.w_out, M, h, f, ed);
+        nl += 6;
+        if (l + 1 < c.num_layers) {
+            norm_bf16(x, nullptr, M, h, xn, rms, eps, s);
+            ++nl;
+        }
+    }
+    if (a.hidden_out) TKV_CUDA_CHECK(cudaMemcpyAsync(a.hidden_out, x, size_t(M) * h * 4, cudaMemcpyDeviceToDevice, s));
+    if (a.n_logit_rows > 0 && a.logits_out) {
+        norm_bf16(x, a.logit_rows, a.n_logit_rows, h, xn, rms, eps, s);
+        EpiParams eh;
+        eh.kind = Epi::store_f32;
+        eh.out = a.logits_out;
+        eh.ldo = c.vocab_padded();
+        run_gemm(xn, head_, a.n_logit_rows, c.vocab_padded(), h, eh);
+        nl += 2;
+        if (a.argmax_out) {
+            argmax_rows(a.logits_out, a.n_logit_rows, c.vocab, c.vocab_padded(), a.argmax_out, nullptr, s);
+            ++nl;
+        }
+    }
+    launches_ = nl;
+}
+
+void Model::forward_ref(const FwdArgs& a, cudaStream_t s) {
+    const ModelCfg& c = cfg_;
+    const DType dt = c.dtype;
+    const size_t es = dtype_size(dt);
+    const int M = a.M, h = c.hidden(), qd = c.num_heads * c.head_dim, kvd = c.kv_dim(), f = c.ffn;
+    uint8_t* p = static_cast<uint8_t*>(ws_);
+    auto take = [&](size_t elems) {
+        void* r = p;
+        p += (elems * es + 255) & ~size_t(255);
+        return r;
+    };
+    const long R = ws_rows_;
+    void* x = take(size_t(R) * h);
+    void* xn = take(size_t(R) * h);
+    void* q = take(size_t(R) * qd);
+    void* k = take(size_t(R) * kvd);
+    void* v = take(size_t(R) * kvd);
+    void* att = take(size_t(R) * qd);
+    void* proj = take(size_t(R) * h);
+    void* mid = take(size_t(R) * f);
+    void* gate = take(size_t(R) * f);
+    const int rms = c.norm == 1;
+    long nl = 0;
+
+    launch_embed(emb_, dt, a.tokens, M, h, x, s);
+    for (int l = 0; l < c.num_layers; ++l) {
+        const Layer& L = layers_[l];
+        void* v_l = a.v_out ? static_cast<uint8_t*>(a.v_out) + size_t(l) * M * kvd * es : v;
+        launch_layer_norm_ref(x, xn, dt, M, h, rms, c.eps, s);
+        launch_matmul_ref(L.wq, xn, q, dt, qd, h, M, 0, s);
+        launch_matmul_ref(L.wk, xn, k, dt, kvd, h, M, 0, s);
+        launch_matmul_ref(L.wv, xn, v_l, dt, kvd, h, M, 0, s);
+        if (a.kraw_out)
+            TKV_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(a.kraw_out) + size_t(l) * M * kvd * es, k,
+                                           size_t(M) * kvd * es, cudaMemcpyDeviceToDevice, s));
+        launch_rope_ref(q, dt, a.pos64, M, c.num_heads, c.head_dim, rope_.cos_d(), rope_.sin_d(), rope_.max_pos(), s);
+        launch_rope_ref(k, dt, a.pos64, M, c.kv_heads, c.head_dim, rope_.cos_d(), rope_.sin_d(), rope_.max_pos(), s);
+        const size_t ctx_off = size_t(l) * a.ctx_rows * kvd * es;
+        const void* kc = a.ctx_k ? static_cast<const uint8_t*>(a.ctx_k) + ctx_off : k;
+        const void* vc = a.ctx_v ? static_cast<const uint8_t*>(a.ctx_v) + ctx_off : v_l;
+        launch_attend_ref(q, k, v_l, kc, vc, a.group, a.seqs, a.n_seqs, M, att, dt, c.num_heads, c.kv_heads, c.head_dim,
+                          a.mode, s);
+        launch_matmul_ref(L.wo, att, proj, dt, h, qd, M, 0, s);
+        launch_add_ref(x, proj, dt, long(M) * h, s);
+        launch_layer_norm_ref(x, xn, dt, M, h, rms, c.eps, s);
+        launch_matmul_ref(L.w_in, xn, mid, dt, f, h, M, c.mlp == 0, s);
+        if (c.mlp == 1) {
+            launch_matmul_ref(L.w_gate, xn, gate, dt, f, h, M, 1, s);
+            launch_mul_ref(mid, gate, dt, long(M) * f, s);
+        }
+        launch_matmul_ref(L.w_out, mid, proj, dt, h, f, M, 0, s);
+        launch_add_ref(x, proj, dt, long(M) * h, s);
+        nl += 15;
+    }
+    if (a.hidden_out) TKV_CUDA_CHECK(cudaMemcpyAsync(a.hidden_out, x, size_t(M) * h * es, cudaMemcpyDeviceToDevice, s));
+    if (a.n_logit_rows > 0 && a.logits_out && dt == DType::f32) {
+        // documented head: final norm of the row, untied head, f32 logits
+        for (int r = 0; r < a.n_logit_rows; ++r) {
+            const int row = a.logit_rows_host ? a.logit_rows_host[r] : M - 1;
+            launch_layer_norm_ref(static_cast<const uint8_t*>(x) + size_t(row) * h * es, xn, dt, 1, h, rms, c.eps, s);
+            launch_matmul_ref(head_, xn, a.logits_out + size_t(r) * c.vocab_padded(), dt, c.vocab, h, 1, 0, s);
+            nl += 2;
+        }
+        if (a.argmax_out) {
+            argmax_rows(a.logits_out, a.n_logit_rows, c.vocab, c.vocab_padded(), a.argmax_out, nullptr, s);
+            ++nl;
+        }
+    }
+    launches_ = nl;
+}
+
+}  // namespace tkv

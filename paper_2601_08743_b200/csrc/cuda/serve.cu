@@ -1,0 +1,471 @@
+// GPU executor (see serve.cuh). The host computes the canonical trace with the reference's
+// exact cache decisions (tablekv::build_trace over a metadata-only slow tier), then replays it:
+// every miss / prefetch becomes a page copy from the pinned arena into the HBM pool (demand
+// loads on one copy stream, prefetches on another so they overlap the current window's
+// compute), evicted tables' pages are recycled only after the compute that may read them.
+// Each window of b_c queries is one gather + one batched prefill on the compute stream.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <numeric>
+
+#include "common.cuh"
+#include "serve.cuh"
+
+namespace tkv {
+
+namespace {
+
+// Slow tier that only knows token counts: the policy trace needs no tensor bytes.
+class MetaTier : public tablekv::SlowTier {
+   public:
+    explicit MetaTier(const Arena& a) : arena_(a) {}
+    bool contains(int id) const override { return arena_.find(id) != nullptr; }
+    std::shared_ptr<const tablekv::TableKV<float>> load(int id) override {
+        auto it = cache_.find(id);
+        if (it != cache_.end()) return it->second;
+        const TableImage* img = arena_.find(id);
+        if (!img) throw tablekv::Error(tablekv::Errc::unknown_table, "table " + std::to_string(id) + " not in the arena");
+        auto kv = std::make_shared<tablekv::TableKV<float>>();
+        kv->table_id = id;
+        kv->token_count = img->tokens;
+        cache_.emplace(id, kv);
+        return kv;
+    }
+
+   private:
+    const Arena& arena_;
+    std::unordered_map<int, std::shared_ptr<const tablekv::TableKV<float>>> cache_;
+};
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct EventPool {
+    std::vector<cudaEvent_t> evs;
+    size_t used = 0;
+    cudaEvent_t get() {
+        if (used == evs.size()) {
+            cudaEvent_t e;
+            TKV_CUDA_CHECK(cudaEventCreate(&e));
+            evs.push_back(e);
+        }
+        return evs[used++];
+    }
+    ~EventPool() {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+}  // namespace
+
+Server::Server(Model& model, Arena& arena, PagePool& pool) : model_(model), arena_(arena), pool_(pool) {
+    int lo, hi;
+    TKV_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, hi));
+    TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&ds_, cudaStreamNonBlocking, hi));
+    TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&ps_, cudaStreamNonBlocking, lo));
+}
+
+Server::~Server() {
+    cudaDeviceSynchronize();
+    cudaFree(ctx_buf_);
+    cudaStreamDestroy(cs_);
+    cudaStreamDestroy(ds_);
+    cudaStreamDestroy(ps_);
+}
+
+void Server::set_table_tokens(std::vector<std::vector<int32_t>> tt, std::vector<int> group_of) {
+    table_tokens_ = std::move(tt);
+    group_of_ = std::move(group_of);
+}
+
+void Server::ensure_ctx(size_t bytes) {
+    if (bytes <= ctx_cap_) return;
+    TKV_CUDA_CHECK(cudaDeviceSynchronize());
+    cudaFree(ctx_buf_);
+    ctx_cap_ = std::max(bytes, ctx_cap_ * 2);
+    TKV_CUDA_CHECK(cudaMalloc(&ctx_buf_, ctx_cap_));
+}
+
+ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOptions& opts) {
+    ServeResult R;
+    if (queries.empty()) return R;
+    const ModelCfg& mc = model_.cfg();
+    const int L = mc.num_layers, kvd = mc.kv_dim();
+    const DType out_dt = mc.dtype == DType::bf16 ? DType::bf16 : DType::f32;
+    const size_t oes = dtype_size(out_dt);
+    const size_t P = pool_.page_bytes();
+    EventPool evp;
+    const double host0 = now_ms();
+    cudaEvent_t t0 = evp.get();
+    TKV_CUDA_CHECK(cudaEventRecord(t0, cs_));
+    TKV_CUDA_CHECK(cudaStreamWaitEvent(ds_, t0));
+    TKV_CUDA_CHECK(cudaStreamWaitEvent(ps_, t0));
+
+    // ---- host: records, rerank, schedule, canonical trace (reference decisions)
+    int n_bits = 0;
+    for (const auto& q : queries)
+        for (int t : q.tables) n_bits = std::max(n_bits, t + 1);
+    std::vector<tablekv::QueryRecord> recs;
+    recs.reserve(queries.size());
+    for (const auto& q : queries) {
+        auto r = tablekv::make_query_record(q.id, {}, q.tables, std::max(1, n_bits), int(q.suffix.size()));
+        r.tables = q.tables;
+        recs.push_back(std::move(r));
+    }
+    R.order = tablekv::serving_order(recs, opts.run);
+    std::vector<tablekv::SimQuery> sims;
+    for (size_t i : R.order) sims.push_back({queries[i].id, queries[i].tables, int(queries[i].suffix.size())});
+    const tablekv::BatchPlan plan = tablekv::schedule(std::move(sims), opts.run.b_c, opts.run.b_m);
+    auto meta = std::make_shared<MetaTier>(arena_);
+    tablekv::TieredCache cache(opts.run.capacity, opts.run.policy, meta);
+    const tablekv::Trace tr = tablekv::build_trace(plan, opts.cost, cache);
+    R.counters = cache.counters();
+
+    // ---- sizing: context slab for the largest window, rope table for the longest row
+    long max_ctx_rows = 0;
+    int max_pos = 1;
+    for (const auto& w : plan.windows) {
+        long rows = 0;
+        for (size_t qi = w.begin; qi < w.end; ++qi) {
+            long c = 0;
+            for (int t : plan.queries[qi].tables) c += arena_.find(t)->tokens;
+            rows += c;
+            max_pos = std::max<int>(max_pos, int(c + long(queries[R.order[qi]].suffix.size()) + 1));
+        }
+        max_ctx_rows = std::max(max_ctx_rows, rows);
+    }
+    model_.rope().ensure(max_pos);
+    ensure_ctx(std::max<size_t>(256, size_t(2) * L * size_t(max_ctx_rows) * kvd * oes));
+    uint8_t* ctx_k = static_cast<uint8_t*>(ctx_buf_);
+    uint8_t* ctx_v = ctx_k + size_t(L) * size_t(max_ctx_rows) * kvd * oes;
+    int32_t* d_argmax = nullptr;
+    float* d_logits = nullptr;
+    const int vp = mc.vocab_padded();
+    size_t max_q = 0;
+    for (const auto& w : plan.windows) max_q = std::max(max_q, w.end - w.begin);
+    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_argmax), sizeof(int32_t) * queries.size(), cs_));
+    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_logits), sizeof(float) * max_q * vp, cs_));
+    std::vector<float> logits_host;
+    if (opts.keep_logits) logits_host.resize(queries.size() * size_t(vp));
+
+    // ---- physical replay
+    std::unordered_map<int, std::vector<int32_t>> resident;
+    const bool managed = opts.run.capacity > 0;
+    auto load = [&](int t, cudaStream_t st) {
+        const TableImage* img = arena_.find(t);
+        std::vector<int32_t> pages = pool_.alloc(int((img->bytes + P - 1) / P));
+        copy_table_to_pages(*img, pool_, pages, opts.engine, opts.sm_copy_ctas, st);
+        R.h2d_bytes += img->bytes;
+        return pages;
+    };
+    std::vector<cudaEvent_t> win_end(plan.windows.size());
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dspan, pspan;
+    cudaEvent_t prev_pref = nullptr;
+    R.window_of.assign(plan.queries.size(), 0);
+    R.argmax.assign(plan.queries.size(), -1);
+
+    for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
+        const auto& w = plan.windows[wi];
+        const auto& wt = tr.windows[wi];
+        std::vector<std::vector<int32_t>> dropped;  // evicted this window: recycle after compute(wi)
+        auto evict = [&](int victim) {
+            if (victim < 0) return;
+            auto it = resident.find(victim);
+            if (it != resident.end()) {
+                dropped.push_back(std::move(it->second));
+                resident.erase(it);
+            }
+        };
+        cudaEvent_t d0 = evp.get(), p0 = evp.get();
+        TKV_CUDA_CHECK(cudaEventRecord(d0, ds_));
+        TKV_CUDA_CHECK(cudaEventRecord(p0, ps_));
+        for (const auto& r : wt.boundary) {
+            R.trace.push_back({int(wi), 0, -1, r.table, r.evicted, r.miss, 0});
+            if (!r.miss) continue;
+            evict(r.evicted);
+            resident[r.table] = load(r.table, ds_);
+            R.trace.back().bytes = arena_.find(r.table)->bytes;
+        }
+        for (const auto& r : wt.prefetch) {
+            R.trace.push_back({int(wi), 1, -1, r.table, r.evicted, true, arena_.find(r.table)->bytes});
+            evict(r.evicted);
+            resident[r.table] = load(r.table, ps_);
+        }
+        // per query: emergency reloads, then a snapshot of its tables' pages
+        struct Seg {
+            int table, tokens;
+            std::vector<int32_t> pages;
+        };
+        std::vector<std::vector<Seg>> qsegs(w.end - w.begin);
+        for (size_t qi = w.begin; qi < w.end; ++qi) {
+            std::unordered_map<int, std::vector<int32_t>> local;  // capacity 0: load-through copies
+            for (const auto& r : wt.emergency[qi - w.begin]) {
+                R.trace.push_back({int(wi), 2, long(qi), r.table, r.evicted, true, arena_.find(r.table)->bytes});
+                evict(r.evicted);
+                auto pages = load(r.table, ds_);
+                if (managed)
+                    resident[r.table] = std::move(pages);
+                else
+                    local[r.table] = std::move(pages);
+            }
+            for (int t : plan.queries[qi].tables) {
+                const auto& pg = managed ? resident.at(t) : local.at(t);
+                qsegs[qi - w.begin].push_back({t, arena_.find(t)->tokens, pg});
+            }
+            if (!managed)
+                for (auto& kv : local) dropped.push_back(std::move(kv.second));
+        }
+        cudaEvent_t d1 = evp.get(), p1 = evp.get();
+        TKV_CUDA_CHECK(cudaEventRecord(d1, ds_));
+        TKV_CUDA_CHECK(cudaEventRecord(p1, ps_));
+        dspan.push_back({d0, d1});
+        pspan.push_back({p0, p1});
+
+        // ---- compute(wi): needs this window's demand loads and every earlier prefetch
+        TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, d1));
+        if (prev_pref) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, prev_pref));
+        prev_pref = p1;
+
+        std::vector<GatherSeg> segs;
+        std::vector<int32_t> page_ids, tokens, pos, logit_rows;
+        std::vector<int64_t> pos64;
+        std::vector<AttnSeq> seqs;
+        std::vector<size_t> seq_query;
+        int ctx_rows = 0, M = 0;
+        for (size_t qi = w.begin; qi < w.end; ++qi) {
+            const ServeQuery& q = queries[R.order[qi]];
+            R.window_of[qi] = int(wi);
+            int cursor = 0;
+            const int q_ctx0 = ctx_rows;
+            for (const Seg& s : qsegs[qi - w.begin]) {
+                segs.push_back({int32_t(page_ids.size()), s.tokens, cursor, ctx_rows});
+                page_ids.insert(page_ids.end(), s.pages.begin(), s.pages.end());
+                cursor += s.tokens;
+                ctx_rows += s.tokens;
+            }
+            R.total_ctx_tokens += cursor;
+            if (q.suffix.empty()) continue;  // nothing to prefill, no first token
+            seqs.push_back({M, int(q.suffix.size()), q_ctx0, cursor});
+            seq_query.push_back(qi);
+            for (size_t i = 0; i < q.suffix.size(); ++i) {
+                tokens.push_back(q.suffix[i]);
+                pos.push_back(cursor + int(i));
+                pos64.push_back(cursor + int64_t(i));
+            }
+            M += int(q.suffix.size());
+            logit_rows.push_back(M - 1);
+        }
+        R.total_suffix_tokens += M;
+        StagingRing& ring = model_.ring();
+        if (ctx_rows > 0) {
+            auto* d_segs = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
+            auto* d_pages = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
+            R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
+            DType in_dt = DType::f32;  // the arena holds one dtype per corpus (f32 .kv files or bf16 encodes)
+            for (const auto& qs : qsegs)
+                if (!qs.empty()) {
+                    in_dt = arena_.find(qs.front().table)->dtype;
+                    break;
+                }
+            cudaEvent_t g0 = nullptr, g1 = nullptr;
+            if (opts.time_kernels) {
+                g0 = evp.get();
+                g1 = evp.get();
+                TKV_CUDA_CHECK(cudaEventRecord(g0, cs_));
+            }
+            launch_gather_rope(pool_.base(), P, d_pages, d_segs, int(segs.size()), ctx_rows, L, kvd, mc.head_dim, in_dt,
+                               out_dt, model_.rope().cos_d(), model_.rope().sin_d(), model_.rope().cos_f(),
+                               model_.rope().sin_f(), ctx_k, ctx_v, max_ctx_rows, cs_);
+            R.launches += 1;
+            if (opts.time_kernels) {
+                TKV_CUDA_CHECK(cudaEventRecord(g1, cs_));
+                R.gather_bytes += double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt) + oes);
+                model_.add_timed(g0, g1, -1.0);  // tagged gather
+            }
+        }
+        if (M > 0) {
+            FwdArgs fa;
+            fa.M = M;
+            fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
+            fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
+            fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
+            fa.n_seqs = int(seqs.size());
+            fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
+            fa.seqs_host = seqs.data();
+            fa.mode = 0;
+            fa.ctx_k = ctx_k;
+            fa.ctx_v = ctx_v;
+            fa.ctx_rows = max_ctx_rows;
+            fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+            fa.n_logit_rows = int(logit_rows.size());
+            fa.logits_out = d_logits;
+            fa.argmax_out = d_argmax + w.begin;  // compacted per window; remapped below
+            R.meta_bytes += tokens.size() * 16 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
+            model_.set_timing(opts.time_kernels);
+            model_.forward(fa, cs_);
+            R.launches += model_.launches();
+            if (opts.keep_logits) {
+                for (size_t k = 0; k < seq_query.size(); ++k)
+                    TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
+                                                   sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
+                TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+            }
+        }
+        win_end[wi] = evp.get();
+        TKV_CUDA_CHECK(cudaEventRecord(win_end[wi], cs_));
+        for (auto& pg : dropped) pool_.release(pg, cs_);
+        // the k-th prefilling query of this window writes its argmax to d_argmax[w.begin + k]
+        for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(w.begin + k);  // slot, resolved below
+    }
+    R.host_ms = now_ms() - host0;
+    TKV_CUDA_CHECK(cudaStreamSynchronize(ps_));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(ds_));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+    std::vector<int32_t> am(queries.size());
+    TKV_CUDA_CHECK(cudaMemcpy(am.data(), d_argmax, sizeof(int32_t) * queries.size(), cudaMemcpyDeviceToHost));
+    for (auto& a : R.argmax)
+        if (a >= 0) a = am[size_t(a)];
+    R.ttft_ms.resize(plan.queries.size());
+    R.window_end_ms.resize(plan.windows.size());
+    for (size_t wi = 0; wi < plan.windows.size(); ++wi) R.window_end_ms[wi] = elapsed(t0, win_end[wi]);
+    for (size_t qi = 0; qi < plan.queries.size(); ++qi) R.ttft_ms[qi] = R.window_end_ms[size_t(R.window_of[qi])];
+    R.makespan_ms = R.window_end_ms.back();
+    for (size_t i = 0; i < dspan.size(); ++i) R.copy_busy_ms += elapsed(dspan[i].first, dspan[i].second) + elapsed(pspan[i].first, pspan[i].second);
+    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
+    if (opts.keep_logits) R.logits = std::move(logits_host);
+    TKV_CUDA_CHECK(cudaFree(d_argmax));
+    TKV_CUDA_CHECK(cudaFree(d_logits));
+    return R;
+}
+
+ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const ServeOptions& opts) {
+    ServeResult R;
+    if (queries.empty()) return R;
+    if (table_tokens_.empty()) throw std::invalid_argument("serve_nocache needs set_table_tokens()");
+    const ModelCfg& mc = model_.cfg();
+    const int vp = mc.vocab_padded();
+    EventPool evp;
+    const double host0 = now_ms();
+    cudaEvent_t t0 = evp.get();
+    TKV_CUDA_CHECK(cudaEventRecord(t0, cs_));
+    int n_bits = 0;
+    for (const auto& q : queries)
+        for (int t : q.tables) n_bits = std::max(n_bits, t + 1);
+    std::vector<tablekv::QueryRecord> recs;
+    for (const auto& q : queries) {
+        auto r = tablekv::make_query_record(q.id, {}, q.tables, std::max(1, n_bits), int(q.suffix.size()));
+        r.tables = q.tables;
+        recs.push_back(std::move(r));
+    }
+    R.order = tablekv::serving_order(recs, opts.run);
+    const size_t n = queries.size(), bc = size_t(opts.run.b_c);
+    int max_pos = 1;
+    for (const auto& q : queries) {
+        long c = long(q.suffix.size()) + 1;
+        for (int t : q.tables) c += long(table_tokens_[size_t(t)].size());
+        max_pos = std::max<int>(max_pos, int(c));
+    }
+    model_.rope().ensure(max_pos);
+    int32_t* d_argmax = nullptr;
+    float* d_logits = nullptr;
+    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_argmax), sizeof(int32_t) * n, cs_));
+    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_logits), sizeof(float) * bc * vp, cs_));
+    std::vector<float> logits_host;
+    if (opts.keep_logits) logits_host.resize(n * size_t(vp));
+    R.window_of.assign(n, 0);
+    R.argmax.assign(n, -1);
+    std::vector<cudaEvent_t> win_end;
+    for (size_t b = 0, wi = 0; b < n; b += bc, ++wi) {
+        const size_t e = std::min(n, b + bc);
+        std::vector<int32_t> tokens, pos, group, logit_rows;
+        std::vector<int64_t> pos64;
+        std::vector<AttnSeq> seqs;
+        std::vector<size_t> seq_query;
+        int M = 0;
+        for (size_t qi = b; qi < e; ++qi) {
+            const ServeQuery& q = queries[R.order[qi]];
+            R.window_of[qi] = int(wi);
+            if (q.suffix.empty()) continue;
+            const int row0 = M;
+            int p = 0;
+            for (int t : q.tables) {
+                for (int32_t tok : table_tokens_[size_t(t)]) {
+                    tokens.push_back(tok);
+                    group.push_back(group_of_[size_t(t)]);
+                    pos.push_back(p);
+                    pos64.push_back(p++);
+                }
+            }
+            R.total_ctx_tokens += p;
+            for (int32_t tok : q.suffix) {
+                tokens.push_back(tok);
+                group.push_back(-1);
+                pos.push_back(p);
+                pos64.push_back(p++);
+            }
+            M += p;
+            seqs.push_back({row0, p, 0, 0});
+            seq_query.push_back(qi);
+            logit_rows.push_back(M - 1);
+        }
+        R.total_suffix_tokens += M;
+        if (M > 0) {
+            StagingRing& ring = model_.ring();
+            FwdArgs fa;
+            fa.M = M;
+            fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
+            fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
+            fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
+            fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
+            fa.n_seqs = int(seqs.size());
+            fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
+            fa.seqs_host = seqs.data();
+            fa.mode = 1;
+            fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+            fa.n_logit_rows = int(logit_rows.size());
+            fa.logits_out = d_logits;
+            fa.argmax_out = d_argmax + b;
+            R.meta_bytes += tokens.size() * 20 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
+            model_.set_timing(opts.time_kernels);
+            model_.forward(fa, cs_);
+            R.launches += model_.launches();
+            if (opts.keep_logits) {
+                for (size_t k = 0; k < seq_query.size(); ++k)
+                    TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
+                                                   sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
+                TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+            }
+            for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(b + k);
+        }
+        win_end.push_back(evp.get());
+        TKV_CUDA_CHECK(cudaEventRecord(win_end.back(), cs_));
+    }
+    R.host_ms = now_ms() - host0;
+    TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+    std::vector<int32_t> am(n);
+    TKV_CUDA_CHECK(cudaMemcpy(am.data(), d_argmax, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    for (auto& a : R.argmax)
+        if (a >= 0) a = am[size_t(a)];
+    R.window_end_ms.resize(win_end.size());
+    for (size_t wi = 0; wi < win_end.size(); ++wi) R.window_end_ms[wi] = elapsed(t0, win_end[wi]);
+    R.ttft_ms.resize(n);
+    for (size_t qi = 0; qi < n; ++qi) R.ttft_ms[qi] = R.window_end_ms[size_t(R.window_of[qi])];
+    R.makespan_ms = R.window_end_ms.back();
+    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
+    if (opts.keep_logits) R.logits = std::move(logits_host);
+    TKV_CUDA_CHECK(cudaFree(d_argmax));
+    TKV_CUDA_CHECK(cudaFree(d_logits));
+    return R;
+}
+
+}  // namespace tkv

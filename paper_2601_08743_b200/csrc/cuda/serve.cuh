@@ -1,0 +1,84 @@
+// GPU executor of the online path: rerank -> schedule -> canonical cache trace (host, exact
+// reference decisions) -> per window: H2D/peer page copies for every miss/prefetch on copy
+// streams, prefix gather+RoPE and the batched suffix prefill + first-token head on the compute
+// stream, events for TTFT. proj/src/pipeline.cpp:310-342 (run_batch) is the reference caller.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "model.cuh"
+#include "runtime.cuh"
+#include "tablekv/pipeline.hpp"
+
+namespace tkv {
+
+struct ServeQuery {
+    std::string id;
+    std::vector<int> tables;       // matched tables in assembly (PK-FK topological) order
+    std::vector<int32_t> suffix;   // remainder tokens (engine.cpp:133-151)
+};
+
+struct ServeOptions {
+    tablekv::RunOptions run;
+    tablekv::CostModel cost;
+    CopyEngine engine = CopyEngine::dma;
+    int sm_copy_ctas = 16;
+    bool keep_logits = false;      // copy first-token logits back (parity tests)
+    bool time_kernels = false;     // per-GEMM events (bench roofline)
+};
+
+struct TraceEvent {  // one cache decision that moved bytes (or a boundary hit)
+    int window, kind;   // kind 0 boundary, 1 prefetch, 2 emergency
+    long query;         // plan-order query index for emergency records, else -1
+    int table, evicted;
+    bool miss;
+    size_t bytes;       // KV bytes copied into HBM for this record
+};
+
+struct ServeResult {
+    std::vector<size_t> order;             // served order (indices into the input)
+    std::vector<double> ttft_ms;           // per served query: batch submission -> first-token logits
+    std::vector<int32_t> argmax;           // per served query: first generated token
+    std::vector<float> logits;             // [served][vocab_padded] when keep_logits
+    std::vector<int> window_of;            // per served query
+    std::vector<double> window_end_ms;
+    std::vector<TraceEvent> trace;
+    tablekv::CacheCounters counters;
+    size_t h2d_bytes = 0, meta_bytes = 0;
+    double copy_busy_ms = 0;               // sum of per-window copy spans (both copy streams)
+    double makespan_ms = 0, host_ms = 0;
+    long launches = 0;
+    double gemm_ms = 0, gemm_flops = 0;    // time_kernels only
+    double gather_ms = 0, gather_bytes = 0;
+    double attn_ms = 0;
+    long total_ctx_tokens = 0, total_suffix_tokens = 0;
+};
+
+class Server {
+   public:
+    Server(Model& model, Arena& arena, PagePool& pool);
+    ~Server();
+    // table_tokens: token ids per table id (needed only by the no-cache baseline)
+    void set_table_tokens(std::vector<std::vector<int32_t>> tt, std::vector<int> group_of);
+    ServeResult serve(const std::vector<ServeQuery>& queries, const ServeOptions& opts);
+    // baseline: full block-masked prefill of [tables ; suffix] per query, no cache, same windows
+    ServeResult serve_nocache(const std::vector<ServeQuery>& queries, const ServeOptions& opts);
+    cudaStream_t compute_stream() const { return cs_; }
+
+   private:
+    void ensure_ctx(size_t bytes);
+    Model& model_;
+    Arena& arena_;
+    PagePool& pool_;
+    cudaStream_t cs_ = nullptr, ds_ = nullptr, ps_ = nullptr;  // compute, demand copies, prefetch copies
+    void* ctx_buf_ = nullptr;
+    size_t ctx_cap_ = 0;
+    std::vector<std::vector<int32_t>> table_tokens_;
+    std::vector<int> group_of_;
+};
+
+}  // namespace tkv
