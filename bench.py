@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""TableCache B200 online-path benchmark (BASELINE.json metric: p50 TTFT and prefill queries/s vs
+no-cache prefill; KV load GB/s vs PCIe).
+
+Workload (default, BASELINE.json configs[1] with the configs[2] model): Spider-like synthetic
+corpus, 40 databases / 200 tables, Zipf popularity, 1000 queries per GPU; Llama-3-8B-shaped
+decoder (32 layers, 32 q / 8 kv heads x 128, SwiGLU 14336, RMSNorm, vocab 128256), random
+(counter-hash) weights, bf16; table KV precomputed offline on the GPU into a pinned host arena;
+LRU fast tier of C = 32 tables over a paged HBM pool; rerank on; b_c = 100, b_m = 10.
+
+One step = one cold-cache batch through the whole online path: global rerank, schedule,
+canonical cache trace, H2D page copies of every miss/prefetch from the pinned arena, prefix
+gather+RoPE and the batched suffix prefill with the first-token head per window.
+`value` = queries/s from CUDA-event makespans (max over ranks); `e2e` = the same batch through
+the C ABI from prompt TEXT (host analysis + D2H of first tokens) by wall clock.
+Multi-GPU (torchrun): one process per GPU, the globally reranked order is cut into contiguous
+slices (weak scaling: 1000 queries per GPU), no collective on the data path.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LLAMA8B = dict(num_layers=32, num_heads=32, num_kv_heads=8, head_dim=128, ffn_dim=14336, vocab_size=128256,
+               mlp="swiglu", norm="rms")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def pct(v, p):
+    v = sorted(v)
+    if not v:
+        return 0.0
+    i = p * (len(v) - 1)
+    lo = int(i)
+    hi = min(lo + 1, len(v) - 1)
+    return v[lo] + (v[hi] - v[lo]) * (i - lo)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in self.rows if r[7] not in ("0", "[N/A]")] or self.rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(loaded)}
+
+
+def build_workload(cfg_name, n_queries_total):
+    from paper_2601_08743_b200 import workloads as W
+    spec = W.CONFIGS[cfg_name]
+    spec = W.SpiderSpec(**{**spec.__dict__, "n_queries": n_queries_total})
+    tables, entries, _ = W.spider_like(spec)
+    return tables, entries
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU path (oracle/_ref/ref_bench, the unchanged
+    reference library) on this host's cores, same metric/unit, bounded sample per step."""
+    if rank != 0:
+        return
+    import multiprocessing
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    threads = multiprocessing.cpu_count()
+    tables, entries = build_workload(args.config, 1000)
+    from paper_2601_08743_b200 import native as N
+    from paper_2601_08743_b200 import workloads as W
+    eng = N.Engine(corpus_json=W.dump_schema_corpus(tables))
+    samples = []
+    for _, text in entries[:threads]:
+        a = eng.analyze(text)
+        nctx = sum(len(eng.info["table_tokens"][t]) for t in a["assembly_order"])
+        samples.append("%d:%d" % (nctx, len(a["remainder"])))
+    if not os.path.exists(exe):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
+        return
+    L = LLAMA8B["num_layers"]
+    per_q = []
+    walls = []
+    for step in range(args.warmup + args.steps):
+        out = subprocess.run([exe, "wide", "32", "128", str(threads)] + samples, capture_output=True, text=True,
+                             check=True)
+        r = json.loads(out.stdout)
+        if step >= args.warmup:
+            per_q += [c * L for c in r["cached_s"]]
+            walls.append(r["cached_wall_s"] * L)
+    qps = len(samples) * len(walls) / sum(walls)
+    line = {"metric": "prefill queries/sec (cached path)", "value": qps, "unit": "queries/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "ms_per_step": sum(walls) / len(walls) * 1e3, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c2 Spider-like 40 DBs/200 tables, Zipf, Llama-3-8B-shaped widths",
+                       "sample": "%d queries x 1 layer at hidden 4096 (reference MHA/LN/SiLU arch), x%d layers" % (len(samples), L)},
+            "p50_ttft_ms": pct(per_q, 0.5) * 1e3, "p99_ttft_ms": pct(per_q, 0.99) * 1e3,
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                             "sample": "%d queries of the c2 workload, query_attend of 1 layer at hidden 4096 "
+                                       "scaled x%d layers (extrapolated)" % (len(samples), L)},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def cpu_baseline_sample(eng, entries, n=4):
+    """Bounded CPU baseline on this host (rank 0, N=1): the unchanged reference library timing one
+    layer of query_attend at hidden 4096 for n queries in parallel, extrapolated to 32 layers."""
+    import multiprocessing
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    threads = min(multiprocessing.cpu_count(), max(1, n))
+    samples = []
+    for _, text in entries[:threads]:
+        a = eng.analyze(text)
+        nctx = sum(len(eng.info["table_tokens"][t]) for t in a["assembly_order"])
+        samples.append("%d:%d" % (nctx, len(a["remainder"])))
+    out = subprocess.run([exe, "wide", "32", "128", str(threads)] + samples, capture_output=True, text=True, check=True)
+    r = json.loads(out.stdout)
+    L = LLAMA8B["num_layers"]
+    qps = len(samples) / (r["cached_wall_s"] * L)
+    return {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+            "sample": "%d c2 queries, reference query_attend of 1 layer at hidden 4096 (MHA/LN/SiLU), x%d layers, "
+                      "%d threads (extrapolated)" % (len(samples), L, threads),
+            "p50_query_ms": pct(r["cached_s"], 0.5) * L * 1e3}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--queries", type=int, default=1000, help="queries per GPU")
+    ap.add_argument("--layers", type=int, default=LLAMA8B["num_layers"])
+    ap.add_argument("--capacity", type=int, default=32)
+    ap.add_argument("--b_c", type=int, default=100)
+    ap.add_argument("--b_m", type=int, default=10)
+    ap.add_argument("--copy-engine", type=int, default=0)
+    ap.add_argument("--nocache-queries", type=int, default=300, help="queries in the no-cache comparison")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2601_08743_b200 import native as N
+    from paper_2601_08743_b200 import workloads as W
+
+    # ---- setup (untimed): corpus, engine, device model, offline table encode into the arena
+    tables, entries = build_workload(args.config, args.queries * world)
+    eng = N.Engine(corpus_json=W.dump_schema_corpus(tables))
+    mk = dict(LLAMA8B, num_layers=args.layers)
+    t0 = time.time()
+    model = N.Model(dtype="bf16", device=local, **mk)
+    store = N.Store(model, page_bytes=2 << 20, n_pages=12288)
+    store.precompute(eng)
+    store.bind_engine(eng)
+    setup_s = time.time() - t0
+    analyzed = [eng.analyze(text, qid) for qid, text in entries]
+    n_bits = len(tables)
+    pcie = N.measure_h2d(256 << 20, 5, local)
+
+    def global_order():
+        return N.rerank([a["assembly_order"] for a in analyzed], n_bits, seed=1)
+
+    def my_slice(order):
+        per = len(order) // world
+        return order[rank * per:(rank + 1) * per]
+
+    opts = N.serve_options(rerank_on=0, pipeline_on=1, capacity=args.capacity, policy="lru", b_c=args.b_c,
+                           b_m=args.b_m, copy_engine=args.copy_engine, time_kernels=1)
+
+    def step():
+        sl = my_slice(global_order())  # global rerank inside the step, on every rank
+        qs = [(analyzed[i]["assembly_order"], analyzed[i]["remainder"]) for i in sl]
+        return store.serve(qs, opts)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    results = []
+    with ClockSampler(local) as clocks:
+        tw = time.perf_counter()
+        for _ in range(args.steps):
+            results.append(step())
+        barrier()
+        wall = time.perf_counter() - tw
+    dev_ms = sum(r["makespan_ms"] for r in results)
+    total_ms = dev_ms
+    if world > 1:
+        t = torch.tensor([dev_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    n_local = len(results[0]["order"])
+    value = n_local * world * args.steps / (total_ms / 1e3)
+    ttfts = [t for r in results for t in r["ttft_ms"]]
+    h2d = sum(r["h2d_bytes"] for r in results) / args.steps
+    copy_ms = sum(r["copy_busy_ms"] for r in results) / args.steps
+    gemm_ms = sum(r["gemm_ms"] for r in results)
+    gemm_fl = sum(r["gemm_flops"] for r in results)
+    launches = sum(r["launches"] for r in results)
+
+    # ---- no-cache baseline on the same kernels (block-masked full prefill), subset
+    nc_n = min(args.nocache_queries, n_local)
+    sl = my_slice(global_order())[:nc_n]
+    qs_nc = [(analyzed[i]["assembly_order"], analyzed[i]["remainder"]) for i in sl]
+    nc_opts = N.serve_options(rerank_on=0, capacity=args.capacity, b_c=args.b_c, b_m=args.b_m, nocache=1)
+    store.serve(qs_nc, nc_opts)  # warm-up
+    nc = store.serve(qs_nc, nc_opts)
+    cached_sub = store.serve(qs_nc, N.serve_options(rerank_on=0, capacity=args.capacity, b_c=args.b_c,
+                                                    b_m=args.b_m))
+    # ---- e2e: prompt text in, first tokens out, through the C ABI (wall clock)
+    e2e_texts = [entries[i][1] for i in my_slice(global_order())]
+    te = time.perf_counter()
+    e2e_res = store.serve_text(eng, e2e_texts, options=N.serve_options(rerank_on=1, capacity=args.capacity,
+                                                                        b_c=args.b_c, b_m=args.b_m))
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_h2d = e2e_res["h2d_bytes"] + e2e_res["meta_bytes"] + sum(len(x.encode()) for x in e2e_texts)
+    e2e_d2h = 4 * len(e2e_res["argmax"])
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    achieved_tf = gemm_fl / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(eng, entries, n=8)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unavailable": str(e)}
+    nc_p50, c_p50 = pct(nc["ttft_ms"], 0.5), pct(cached_sub["ttft_ms"], 0.5)
+    line = {
+        "metric": "prefill queries/sec (cached path); p50/p99 TTFT vs no-cache prefill; KV load GB/s vs PCIe",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "%s Spider-like: %d DBs / %d tables, Zipf(1.1), %d queries per GPU; Llama-3-8B-shaped "
+                               "(%d layers, 32q/8kv x128, SwiGLU 14336, RMSNorm, vocab 128256), random weights"
+                               % (args.config, W.CONFIGS[args.config].n_db, len(tables), n_local, args.layers),
+                   "cache": "LRU C=%d tables, b_c=%d, b_m=%d, rerank on, 2 MiB HBM pages" % (args.capacity, args.b_c, args.b_m),
+                   "parallelism": "dp%d (request slices of the global rerank)" % world,
+                   "l2": "inputs larger than L2 (16 GB weights streamed per window)"},
+        "p50_ttft_ms": pct(ttfts, 0.5), "p99_ttft_ms": pct(ttfts, 0.99),
+        "nocache": {"queries": nc_n, "p50_ttft_ms": nc_p50, "p99_ttft_ms": pct(nc["ttft_ms"], 0.99),
+                    "qps": nc_n / (nc["makespan_ms"] / 1e3), "cached_p50_ttft_ms_same_subset": c_p50,
+                    "cached_qps_same_subset": nc_n / (cached_sub["makespan_ms"] / 1e3),
+                    "p50_ttft_reduction": nc_p50 / c_p50 if c_p50 else None,
+                    "argmax_agreement": float(np.mean([a == b for a, b in zip(nc["argmax"], cached_sub["argmax"])]))},
+        "kv_load": {"bytes_per_step": h2d, "copy_busy_ms_per_step": copy_ms,
+                    "gbs": h2d / (copy_ms / 1e3) / 1e9 if copy_ms else None, "pcie_h2d_peak_gbs": pcie,
+                    "frac_of_pcie": (h2d / (copy_ms / 1e3) / 1e9) / pcie if copy_ms else None,
+                    "hits_misses_swaps_prefetch": results[0]["counters"]},
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
+                     "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                     "share_of_step": gemm_ms / dev_ms if dev_ms else None},
+        "gather": {"ms_per_step": sum(r["gather_ms"] for r in results) / args.steps},
+        "attention_ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
+        "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,
+                "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+        "setup_s": setup_s, "wall_s_timed": wall,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,10 +178,15 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         const auto& w = plan.windows[wi];
         const auto& wt = tr.windows[wi];
         std::vector<std::vector<int32_t>> dropped;  // evicted this window: recycle after compute(wi)
+        // Pages of tables evicted during this window stay readable until compute(wi) is done.
+        // The reference trace lets a query's own emergency get evict another of its tables
+        // without reloading it (pipeline.cpp:98-107), so snapshots may need them.
+        std::unordered_map<int, std::vector<int32_t>> gone;
         auto evict = [&](int victim) {
             if (victim < 0) return;
             auto it = resident.find(victim);
             if (it != resident.end()) {
+                gone[victim] = it->second;
                 dropped.push_back(std::move(it->second));
                 resident.erase(it);
             }
@@ -219,8 +224,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                     local[r.table] = std::move(pages);
             }
             for (int t : plan.queries[qi].tables) {
-                const auto& pg = managed ? resident.at(t) : local.at(t);
-                qsegs[qi - w.begin].push_back({t, arena_.find(t)->tokens, pg});
+                const std::vector<int32_t>* pg = nullptr;
+                if (!managed) pg = &local.at(t);
+                else if (auto r = resident.find(t); r != resident.end()) pg = &r->second;
+                else pg = &gone.at(t);  // evicted earlier in this window, bytes still intact
+                qsegs[qi - w.begin].push_back({t, arena_.find(t)->tokens, *pg});
             }
             if (!managed)
                 for (auto& kv : local) dropped.push_back(std::move(kv.second));
@@ -307,6 +315,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             fa.ctx_v = ctx_v;
             fa.ctx_rows = max_ctx_rows;
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+            fa.logit_rows_host = logit_rows.data();
             fa.n_logit_rows = int(logit_rows.size());
             fa.logits_out = d_logits;
             fa.argmax_out = d_argmax + w.begin;  // compacted per window; remapped below
@@ -432,6 +441,7 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
             fa.seqs_host = seqs.data();
             fa.mode = 1;
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+            fa.logit_rows_host = logit_rows.data();
             fa.n_logit_rows = int(logit_rows.size());
             fa.logits_out = d_logits;
             fa.argmax_out = d_argmax + b;
