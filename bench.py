@@ -230,6 +230,15 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier()
+    if os.environ.get("TKV_NCU"):
+        # profiling run (never a bench number): capture exactly one serving step under ncu
+        # --profile-from-start off, then exit
+        torch.cuda.cudart().cudaProfilerStart()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        print(json.dumps({"profiled": "one serving step", "queries": args.queries}))
+        return
     results = []
     with ClockSampler(local) as clocks:
         tw = time.perf_counter()

@@ -892,16 +892,21 @@ int tkv_debug_gemm(int M, int N, int K, const uint16_t* A, const uint16_t* B, in
         cudaEvent_t a, b;
         TKV_CUDA_CHECK(cudaEventCreate(&a));
         TKV_CUDA_CHECK(cudaEventCreate(&b));
-        if (simt) tkv::gemm_bf16_simt(dA, dB, M, N, K, ep, nullptr);
-        else tkv::gemm_bf16(dA, dB, M, N, K, ep, nullptr);  // warm-up (tensor map / attributes)
+        // simt: 0 = product kernel (persistent tcgen05), 1 = SIMT reference, 2 = one-tile-per-CTA tcgen05
+        auto run = [&] {
+            if (simt == 1) tkv::gemm_bf16_simt(dA, dB, M, N, K, ep, nullptr);
+            else if (simt == 2) tkv::gemm_bf16_classic(dA, dB, M, N, K, ep, nullptr);
+            else tkv::gemm_bf16(dA, dB, M, N, K, ep, nullptr);
+        };
+        run();  // warm-up (tensor maps, smem attributes)
+        const int reps = simt == 1 ? 1 : 5;
         TKV_CUDA_CHECK(cudaEventRecord(a, nullptr));
-        if (simt) tkv::gemm_bf16_simt(dA, dB, M, N, K, ep, nullptr);
-        else tkv::gemm_bf16(dA, dB, M, N, K, ep, nullptr);
+        for (int r = 0; r < reps; ++r) run();
         TKV_CUDA_CHECK(cudaEventRecord(b, nullptr));
         TKV_CUDA_CHECK(cudaEventSynchronize(b));
         float ms = 0;
         TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
-        if (ms_out) *ms_out = ms;
+        if (ms_out) *ms_out = ms / reps;
         TKV_CUDA_CHECK(cudaMemcpy(C, dC, cb, cudaMemcpyDeviceToHost));
         cudaEventDestroy(a);
         cudaEventDestroy(b);

@@ -265,6 +265,129 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
 }
 
+// ------------------------------------------------------------------ persistent kernel
+// One CTA per SM looping over tiles (static round robin, M-fastest raster: consecutive tiles
+// share the weight tile B while the activation panel A stays L2-resident, so weights stream from
+// HBM once). Warp 0 = TMA producer, warp 1 = MMA issuer, warps 2-5 = epilogue. The accumulator is
+// double-buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of i+1.
+constexpr int kPersistThreads = 192;
+
+template <int BN, int STAGES>
+struct SmemP {
+    static constexpr int a_bytes = BM * BK * 2;
+    static constexpr int b_bytes = BN * BK * 2;
+    static constexpr int stage_bytes = a_bytes + b_bytes;
+    static constexpr int bars_off = STAGES * stage_bytes;
+    static constexpr int n_bars = 2 * STAGES + 4;  // full, empty, tmem_full[2], tmem_empty[2]
+    static constexpr int total = bars_off + n_bars * 8 + 16 + 1024;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kPersistThreads, 1)
+    gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                       int K, const __grid_constant__ EpiParams ep) {
+    using S = SmemP<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::n_bars);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, tiles = mt * nt;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull0 + 8 * i, 1);
+            mbar_init(tempty0 + 8 * i, 4);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 2) {  // 2 accumulators x BN f32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait(empty0 + 8 * st, ((it / STAGES) & 1) ^ 1);
+                    const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+                    mbar_expect_tx(full0 + 8 * st, S::stage_bytes);
+                    tma_load_2d(sa, &tmA, full0 + 8 * st, kb * BK, m0);
+                    tma_load_2d(sa + S::a_bytes, &tmB, full0 + 8 * st, kb * BK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            int it = 0, local = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+                const int acc = local & 1;
+                mbar_wait(tempty0 + 8 * acc, ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(acc * BN);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait(full0 + 8 * st, (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+                    const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + S::a_bytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) tc_mma(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    tc_commit(empty0 + 8 * st);
+                }
+                tc_commit(tfull0 + 8 * acc);
+            }
+        }
+    } else {
+        // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        int local = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+            mbar_wait(tfull0 + 8 * acc, (local >> 1) & 1);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
+                if (m < M && n0 + c < N) epilogue32(ep, m, n0 + c, v);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+}
+
 // ------------------------------------------------------------------ SIMT reference
 __global__ void gemm_simt_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B, int M, int N,
                                  int K, EpiParams ep) {
@@ -324,13 +447,48 @@ void launch_tc(const void* A, const void* B, int M, int N, int K, const EpiParam
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        TKV_CUDA_CHECK(cudaGetDevice(&dev));
+        TKV_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+template <int BN, int STAGES>
+void launch_persistent(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    using S = SmemP<BN, STAGES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            S::total));
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map_2d(A, M, K, BM);
+    const CUtensorMap tb = make_map_2d(B, N, K, BN);
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    gemm_tc_persistent<BN, STAGES><<<std::min(tiles, sm_count()), kPersistThreads, S::total, s>>>(ta, tb, M, N, K, ep);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace
 
 void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     if (M == 0) return;
     if (K % 8 || N % 32) throw std::invalid_argument("gemm_bf16: need K % 8 == 0 and N % 32 == 0");
-    // Wide N with enough rows: 128x256 tiles (one CTA per SM, 4 stages); otherwise 128x128
-    // tiles at 2 CTAs per SM so one CTA's epilogue overlaps the other's main loop.
+    // persistent warp-specialised kernel; 128x256 tiles when N allows, else 128x128 with a deeper ring
+    if (N % 256 == 0)
+        launch_persistent<256, 4>(A, B, M, N, K, ep, s);
+    else
+        launch_persistent<128, 6>(A, B, M, N, K, ep, s);
+}
+
+void gemm_bf16_classic(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    if (M == 0) return;
+    if (K % 8 || N % 32) throw std::invalid_argument("gemm_bf16: need K % 8 == 0 and N % 32 == 0");
+    // one tile per CTA (round-1 kernel), kept for A/B comparisons
     const long tiles256 = long((N + 255) / 256) * ((M + BM - 1) / BM);
     if (N % 256 == 0 && tiles256 >= 2 * kNumSMs)
         launch_tc<256, 4>(A, B, M, N, K, ep, s);

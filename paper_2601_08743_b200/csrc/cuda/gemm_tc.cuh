@@ -35,6 +35,9 @@ struct EpiParams {
 // Launch on stream; A, B device pointers (bf16 bits), K % 8 == 0, N % 32 == 0.
 void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);
 
+// Non-persistent one-tile-per-CTA variant (the first version; A/B comparisons).
+void gemm_bf16_classic(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);
+
 // Simple SIMT bf16 GEMM with the same epilogues (correctness reference for tests only).
 void gemm_bf16_simt(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);
 

@@ -440,7 +440,7 @@ def measure_h2d(bytes_=256 << 20, reps=5, device=0):
     return g.value
 
 
-def debug_gemm(A_bits, B_bits, epilogue=1, simt=False):
+def debug_gemm(A_bits, B_bits, epilogue=1, simt=0):
     A = np.ascontiguousarray(A_bits, dtype=np.uint16)
     B = np.ascontiguousarray(B_bits, dtype=np.uint16)
     M, K = A.shape
