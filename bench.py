@@ -257,6 +257,8 @@ def main():
     ttfts = [t for r in results for t in r["ttft_ms"]]
     h2d = sum(r["h2d_bytes"] for r in results) / args.steps
     copy_ms = sum(r["copy_busy_ms"] for r in results) / args.steps
+    dem_b = sum(r["h2d_demand_bytes"] for r in results) / args.steps
+    dem_ms = sum(r["copy_demand_ms"] for r in results) / args.steps
     gemm_ms = sum(r["gemm_ms"] for r in results)
     gemm_fl = sum(r["gemm_flops"] for r in results)
     launches = sum(r["launches"] for r in results)
@@ -316,8 +318,11 @@ def main():
                     "p50_ttft_reduction": nc_p50 / c_p50 if c_p50 else None,
                     "argmax_agreement": float(np.mean([a == b for a, b in zip(nc["argmax"], cached_sub["argmax"])]))},
         "kv_load": {"bytes_per_step": h2d, "copy_busy_ms_per_step": copy_ms,
-                    "gbs": h2d / (copy_ms / 1e3) / 1e9 if copy_ms else None, "pcie_h2d_peak_gbs": pcie,
-                    "frac_of_pcie": (h2d / (copy_ms / 1e3) / 1e9) / pcie if copy_ms else None,
+                    "demand_bytes_per_step": dem_b, "demand_copy_ms_per_step": dem_ms,
+                    "gbs": dem_b / (dem_ms / 1e3) / 1e9 if dem_ms else None, "pcie_h2d_peak_gbs": pcie,
+                    "frac_of_pcie": (dem_b / (dem_ms / 1e3) / 1e9) / pcie if dem_ms else None,
+                    "gbs_definition": "demand-stream bytes / summed per-window spans of its back-to-back copies",
+                    "copy_engine": ["dma", "sm-16B-kernel"][args.copy_engine],
                     "hits_misses_swaps_prefetch": results[0]["counters"]},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",

@@ -173,6 +173,8 @@ json serve_result_json(const tkv::ServeResult& R) {
             {"h2d_bytes", R.h2d_bytes},
             {"meta_bytes", R.meta_bytes},
             {"copy_busy_ms", R.copy_busy_ms},
+            {"h2d_demand_bytes", R.h2d_demand_bytes},
+            {"copy_demand_ms", R.copy_demand_ms},
             {"makespan_ms", R.makespan_ms},
             {"host_ms", R.host_ms},
             {"launches", R.launches},

@@ -49,7 +49,9 @@ struct ServeResult {
     std::vector<TraceEvent> trace;
     tablekv::CacheCounters counters;
     size_t h2d_bytes = 0, meta_bytes = 0;
+    size_t h2d_demand_bytes = 0;           // boundary + emergency loads (demand copy stream)
     double copy_busy_ms = 0;               // sum of per-window copy spans (both copy streams)
+    double copy_demand_ms = 0;             // demand stream only (its copies run back to back)
     double makespan_ms = 0, host_ms = 0;
     long launches = 0;
     double gemm_ms = 0, gemm_flops = 0;    // time_kernels only
