@@ -207,12 +207,13 @@ def main():
     n_bits = len(tables)
     pcie = N.measure_h2d(256 << 20, 5, local)
 
+    from paper_2601_08743_b200 import sharding as S
+
     def global_order():
-        return N.rerank([a["assembly_order"] for a in analyzed], n_bits, seed=1)
+        return S.global_order([a["assembly_order"] for a in analyzed], n_bits, seed=1)
 
     def my_slice(order):
-        per = len(order) // world
-        return order[rank * per:(rank + 1) * per]
+        return S.rank_slice(order, rank, world)
 
     opts = N.serve_options(rerank_on=0, pipeline_on=1, capacity=args.capacity, policy="lru", b_c=args.b_c,
                            b_m=args.b_m, copy_engine=args.copy_engine, time_kernels=1)
