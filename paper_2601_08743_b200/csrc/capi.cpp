@@ -504,75 +504,27 @@ int tkv_model_forward(tkv_model* m, const int32_t* tokens, const int32_t* positi
         need(mode == 1 || n_ctx == 0 || (ctx_k && ctx_v), "mode 0 with n_ctx > 0 needs ctx_k / ctx_v");
         need(mode == 0 || groups, "mode 1 needs group ids");
         set_device(m->device);
-        tkv::Model& model = *m->m;
-        const auto& c = model.cfg();
+        const auto& c = m->m->cfg();
         for (int i = 0; i < n; ++i)
             if (tokens[i] < 0 || tokens[i] >= c.vocab)
                 throw tablekv::Error(tablekv::Errc::bad_config, "token id " + std::to_string(tokens[i]) + " outside vocabulary");
-        cudaStream_t s = m->s;
-        const size_t es = tkv::dtype_size(c.dtype);
-        const int L = c.num_layers, kvd = c.kv_dim(), h = c.hidden();
-        std::vector<int32_t> pos(static_cast<size_t>(n));
-        for (int i = 0; i < n; ++i) pos[size_t(i)] = positions ? positions[i] : n_ctx + i;
-        std::vector<int64_t> pos64(pos.begin(), pos.end());
-        model.rope().ensure(*std::max_element(pos.begin(), pos.end()) + 2);
-        std::vector<void*> bufs;
-        auto dmalloc = [&](size_t bytes) {
-            void* p = nullptr;
-            TKV_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-            bufs.push_back(p);
-            return p;
-        };
-        auto up = [&](const void* src, size_t bytes) {
-            void* d = dmalloc(bytes);
-            TKV_CUDA_CHECK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
-            return d;
-        };
-        struct Free {
-            std::vector<void*>& b;
-            ~Free() {
-                for (void* p : b) cudaFree(p);
-            }
-        } freer{bufs};
-        tkv::FwdArgs a;
-        a.M = n;
-        a.tokens = static_cast<const int32_t*>(up(tokens, size_t(n) * 4));
-        a.pos = static_cast<const int32_t*>(up(pos.data(), size_t(n) * 4));
-        a.pos64 = static_cast<const int64_t*>(up(pos64.data(), size_t(n) * 8));
-        if (groups) a.group = static_cast<const int32_t*>(up(groups, size_t(n) * 4));
-        const tkv::AttnSeq seq{0, n, 0, mode == 0 ? n_ctx : 0};
-        a.n_seqs = 1;
-        a.seqs = static_cast<const tkv::AttnSeq*>(up(&seq, sizeof(seq)));
-        a.seqs_host = &seq;
-        a.mode = mode;
-        if (mode == 0 && n_ctx > 0) {
-            const size_t cb = size_t(L) * size_t(n_ctx) * kvd * es;
-            a.ctx_k = up(ctx_k, cb);
-            a.ctx_v = up(ctx_v, cb);
-            a.ctx_rows = n_ctx;
-        }
-        const size_t hbytes = size_t(n) * h * (c.dtype == tkv::DType::bf16 ? 4 : es);
-        if (hidden_out) a.hidden_out = dmalloc(hbytes);
-        const size_t kvb = size_t(L) * n * kvd * es;
-        if (kraw_out) a.kraw_out = dmalloc(kvb);
-        if (v_out) a.v_out = dmalloc(kvb);
-        const int32_t last = n - 1;
-        if (logits_out || argmax_out) {
-            need(c.dtype != tkv::DType::f64, "logits are produced by f32 / bf16 models");
-            a.logit_rows = static_cast<const int32_t*>(up(&last, 4));
-            a.logit_rows_host = &last;
-            a.n_logit_rows = 1;
-            a.logits_out = static_cast<float*>(dmalloc(size_t(c.vocab_padded()) * 4));
-            a.argmax_out = static_cast<int32_t*>(dmalloc(4));
-        }
-        model.forward(a, s);
-        if (hidden_out) TKV_CUDA_CHECK(cudaMemcpyAsync(hidden_out, a.hidden_out, hbytes, cudaMemcpyDeviceToHost, s));
-        if (kraw_out) TKV_CUDA_CHECK(cudaMemcpyAsync(kraw_out, a.kraw_out, kvb, cudaMemcpyDeviceToHost, s));
-        if (v_out) TKV_CUDA_CHECK(cudaMemcpyAsync(v_out, a.v_out, kvb, cudaMemcpyDeviceToHost, s));
-        if (logits_out)
-            TKV_CUDA_CHECK(cudaMemcpyAsync(logits_out, a.logits_out, size_t(c.vocab_padded()) * 4, cudaMemcpyDeviceToHost, s));
-        if (argmax_out) TKV_CUDA_CHECK(cudaMemcpyAsync(argmax_out, a.argmax_out, 4, cudaMemcpyDeviceToHost, s));
-        TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+        std::vector<int64_t> pos;
+        if (positions) pos.assign(positions, positions + n);
+        tkv::HostFwd h;
+        h.tokens = tokens;
+        h.positions = positions ? pos.data() : nullptr;
+        h.groups = groups;
+        h.n = n;
+        h.mode = mode;
+        h.n_ctx = mode == 0 ? n_ctx : 0;
+        h.ctx_k = ctx_k;
+        h.ctx_v = ctx_v;
+        h.hidden = hidden_out;
+        h.kraw = kraw_out;
+        h.v = v_out;
+        h.logits = logits_out;
+        h.argmax = argmax_out;
+        tkv::forward_host(*m->m, m->s, h);
     });
 }
 

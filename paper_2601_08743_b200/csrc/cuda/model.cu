@@ -299,6 +299,9 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
                 add_timed(e0, e1, 0.0);
             }
         }
+        if (a.krot_out)
+            TKV_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(a.krot_out) + size_t(l) * M * kvd * 2, k,
+                                           size_t(M) * kvd * 2, cudaMemcpyDeviceToDevice, s));
 
         EpiParams eo;
         eo.kind = Epi::resid_f32;
@@ -382,6 +385,9 @@ void Model::forward_ref(const FwdArgs& a, cudaStream_t s) {
                                            size_t(M) * kvd * es, cudaMemcpyDeviceToDevice, s));
         launch_rope_ref(q, dt, a.pos64, M, c.num_heads, c.head_dim, rope_.cos_d(), rope_.sin_d(), rope_.max_pos(), s);
         launch_rope_ref(k, dt, a.pos64, M, c.kv_heads, c.head_dim, rope_.cos_d(), rope_.sin_d(), rope_.max_pos(), s);
+        if (a.krot_out)
+            TKV_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(a.krot_out) + size_t(l) * M * kvd * es, k,
+                                           size_t(M) * kvd * es, cudaMemcpyDeviceToDevice, s));
         const size_t ctx_off = size_t(l) * a.ctx_rows * kvd * es;
         const void* kc = a.ctx_k ? static_cast<const uint8_t*>(a.ctx_k) + ctx_off : k;
         const void* vc = a.ctx_v ? static_cast<const uint8_t*>(a.ctx_v) + ctx_off : v_l;

@@ -78,6 +78,7 @@ struct FwdArgs {
     long ctx_rows = 0;
     void* kraw_out = nullptr;           // optional [L][M][kv_dim] pre-rotation keys (offline encode)
     void* v_out = nullptr;              // optional [L][M][kv_dim]
+    void* krot_out = nullptr;           // optional [L][M][kv_dim] rotated own keys (prefill's k_rot)
     void* hidden_out = nullptr;         // optional [M][hidden] final hidden (f32 for bf16 path, T otherwise)
     const int32_t* logit_rows = nullptr;  // optional device [n_logit_rows] rows to run the head on
     const int32_t* logit_rows_host = nullptr;  // host copy (reference-precision path)
@@ -85,6 +86,23 @@ struct FwdArgs {
     float* logits_out = nullptr;        // [n_logit_rows][vocab_padded]
     int32_t* argmax_out = nullptr;      // optional [n_logit_rows]
 };
+
+// One sequence through the forward with HOST buffers (the parity wrappers: tkv_model_forward and
+// the C++ attention.hpp templates). Outputs are in the model dtype except hidden for bf16 models
+// (f32 residual stream). positions nullable (= n_ctx + i).
+struct HostFwd {
+    const int32_t* tokens = nullptr;
+    const int64_t* positions = nullptr;
+    const int32_t* groups = nullptr;
+    int n = 0, mode = 0, n_ctx = 0;
+    const void* ctx_k = nullptr;
+    const void* ctx_v = nullptr;
+    void *hidden = nullptr, *kraw = nullptr, *krot = nullptr, *v = nullptr;
+    float* logits = nullptr;  // [vocab_padded] of the last row
+    int32_t* argmax = nullptr;
+};
+class Model;
+void forward_host(Model& m, cudaStream_t s, const HostFwd& h);
 
 class Model {
    public:
