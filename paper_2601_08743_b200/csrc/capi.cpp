@@ -728,6 +728,7 @@ int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, void* 
 int tkv_store_info(const tkv_store* s, size_t* tables, size_t* arena_bytes, size_t* free_pages) {
     return guard([&] {
         need(s, "null argument");
+        s->pool->reclaim();  // fold completed deferred frees back into the free list
         if (tables) *tables = s->arena->size();
         if (arena_bytes) *arena_bytes = s->arena->total_bytes();
         if (free_pages) *free_pages = size_t(s->pool->free_pages());

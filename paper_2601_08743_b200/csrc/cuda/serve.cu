@@ -352,6 +352,9 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         // the k-th prefilling query of this window writes its argmax to d_argmax[w.begin + k]
         for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(w.begin + k);  // slot, resolved below
     }
+    // the batch's cache dies with it: every still-resident table's pages go back to the pool
+    for (auto& kv : resident) pool_.release(kv.second, cs_);
+    resident.clear();
     R.host_ms = now_ms() - host0;
     TKV_CUDA_CHECK(cudaStreamSynchronize(ps_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(ds_));

@@ -233,6 +233,7 @@ def test_executor_replays_reference_trace(f32_store, run_name):
     golden_argmax = {n["query"]: n["argmax"] for n in g["numerics"]}
     assert [res["argmax"][i] for i in range(64)] == [golden_argmax[q] for q in res["order"]]
     assert len(res["ttft_ms"]) == 64 and all(t > 0 for t in res["ttft_ms"])
+    assert f32_store.info()["free_pages"] == 4096  # every page returned once the batch is done
 
 
 def test_executor_nocache_baseline_same_first_tokens(f32_model, f32_store):
