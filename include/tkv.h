@@ -98,6 +98,8 @@ typedef struct {
 } tkv_model_config;
 int tkv_model_create(int device, const tkv_model_config* cfg, tkv_model** out);
 void tkv_model_destroy(tkv_model* m);
+/* attention kernel of bf16 models: 0 tcgen05 where supported (head_dim 128), 1 mma.sync */
+int tkv_model_set_attention(tkv_model* m, int impl);
 /* which: 0 embedding [vocab][hidden], 1 head [vocab(_padded for bf16)][hidden]; raw model-dtype bytes */
 int tkv_model_weights(tkv_model* m, int which, void* host_out, size_t bytes);
 /* One sequence through the device forward with host buffers (the parity wrappers of prefill /

@@ -483,6 +483,13 @@ void tkv_model_destroy(tkv_model* m) {
     delete m;
 }
 
+int tkv_model_set_attention(tkv_model* m, int impl) {
+    return guard([&] {
+        need(m && (impl == 0 || impl == 1), "impl must be 0 (tcgen05) or 1 (mma.sync)");
+        m->m->set_attention_impl(impl);
+    });
+}
+
 int tkv_model_weights(tkv_model* m, int which, void* host_out, size_t bytes) {
     return guard([&] {
         need(m && host_out, "null argument");

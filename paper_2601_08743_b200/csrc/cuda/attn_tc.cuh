@@ -22,8 +22,15 @@ struct AttnArgs {
     float scale;                 // 1/sqrt(d)
 };
 
-// tokens per CTA tile for a GQA ratio (64 rows / G)
+// tokens per CTA tile for a GQA ratio (rows per CTA / G)
 int attn_rows_per_tile(int num_heads, int kv_heads);
 void attention_bf16(const AttnArgs& a, int n_tiles, cudaStream_t s);
+
+// tcgen05 / TMEM / TMA attention (head_dim 128); work items {seq, tok0, kv head} with tok0 stepping
+// by attn_tc5_rows_per_tile; ctx_rows / own_rows = row extents of the k_ctx/v_ctx and k_own/v_own
+// buffers (TMA bounds).
+bool attention_tc5_supported(const AttnArgs& a);
+int attn_tc5_rows_per_tile(int num_heads, int kv_heads);
+void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_rows, long own_rows, cudaStream_t s);
 
 }  // namespace tkv

@@ -93,6 +93,8 @@ Model::Model(const ModelCfg& cfg, cudaStream_t s) : cfg_(cfg), rope_(cfg.head_di
     if (cfg.vocab <= 0) throw std::invalid_argument("vocab must be positive");
     alloc_weights(s);
     rope_.ensure(8192);
+    // TKV_ATTN=mma forces the mma.sync attention kernel everywhere (A/B measurements)
+    if (const char* e = std::getenv("TKV_ATTN"); e && std::string(e) == "mma") attn_impl_ = 1;
 }
 
 Model::~Model() {
@@ -170,6 +172,7 @@ void Model::ensure_ws(int M, cudaStream_t s) {
     // x (f32 or T), xn, q, k, v, attn, proj (T), mid (f), gate (f)
     const size_t per_row = size_t(h) * std::max<size_t>(4, es) + (h + qd + 2 * kvd + qd + h) * es + 2 * size_t(f) * es + 64;
     TKV_CUDA_CHECK(cudaMalloc(&ws_, per_row * cap + 4096));
+    TKV_CUDA_CHECK(cudaMemsetAsync(ws_, 0, per_row * cap + 4096, s));  // finite padding rows for masked tiles
     ws_rows_ = cap;
 }
 
@@ -229,7 +232,12 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
     void* mid = take(size_t(R) * f * 2);
 
     // attention work list: (seq, first token, kv head)
-    const int tq = attn_rows_per_tile(c.num_heads, c.kv_heads);
+    // tcgen05 attention over cached prefixes at head_dim 128 (the Llama-shaped serving path); the
+    // mma.sync kernel for other head dims and for block-mask prefill (mode 1: its per-key group
+    // test runs cheaper there)
+    const int G = c.num_heads / c.kv_heads;
+    const bool use_tc5 = attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0 && a.mode == 0;
+    const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
         for (int t0 = 0; t0 < a.seqs_host[si].n_own; t0 += tq)
@@ -293,7 +301,10 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
                 e1 = timing_event();
                 TKV_CUDA_CHECK(cudaEventRecord(e0, s));
             }
-            attention_bf16(aa, int(tiles.size()), s);
+            if (use_tc5)
+                attention_tc5(aa, d_tiles, int(tiles.size()), a.ctx_k ? a.ctx_rows : 0, M, s);
+            else
+                attention_bf16(aa, int(tiles.size()), s);
             if (timing_) {
                 TKV_CUDA_CHECK(cudaEventRecord(e1, s));
                 add_timed(e0, e1, 0.0);

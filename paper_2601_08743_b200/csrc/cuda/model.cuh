@@ -122,6 +122,9 @@ class Model {
     // Optional CUDA-event timing of every GEMM / attention launch (bench roofline). Records
     // accumulate across forwards until collect_timing(), which needs the stream drained.
     void set_timing(bool on) { timing_ = on; }
+    // attention kernel: 0 = tcgen05 where supported (head_dim 128), 1 = mma.sync everywhere
+    void set_attention_impl(int impl) { attn_impl_ = impl; }
+    int attention_impl() const { return attn_impl_; }
     void add_timed(cudaEvent_t a, cudaEvent_t b, double flops);  // flops < 0 tags a gather
     void collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms);
     cudaEvent_t timing_event();
@@ -136,6 +139,7 @@ class Model {
     std::vector<cudaEvent_t> ev_pool_;
     size_t ev_used_ = 0;
     bool timing_ = false;
+    int attn_impl_ = 0;
 
     struct Layer {
         void *wqkv = nullptr, *wq = nullptr, *wk = nullptr, *wv = nullptr, *wo = nullptr;

@@ -94,6 +94,7 @@ void Server::ensure_ctx(size_t bytes) {
     cudaFree(ctx_buf_);
     ctx_cap_ = std::max(bytes, ctx_cap_ * 2);
     TKV_CUDA_CHECK(cudaMalloc(&ctx_buf_, ctx_cap_));
+    TKV_CUDA_CHECK(cudaMemset(ctx_buf_, 0, ctx_cap_));  // rows past a window's prefix stay finite (masked tiles read them)
 }
 
 ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOptions& opts) {

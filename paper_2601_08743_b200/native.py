@@ -82,6 +82,7 @@ _sig("tkv_run_batch_json", C.c_char_p, C.POINTER(_vp))
 _sig("tkv_model_create", C.c_int, C.POINTER(tkv_model_config), C.POINTER(_vp))
 _sig("tkv_model_destroy", _vp, res=None)
 _sig("tkv_model_weights", _vp, C.c_int, _vp, C.c_size_t)
+_sig("tkv_model_set_attention", _vp, C.c_int)
 _sig("tkv_model_forward", _vp, _i32p, _i32p, _i32p, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp, _fp, _i32p)
 _sig("tkv_store_create", _vp, C.c_size_t, C.c_int, C.POINTER(_vp))
 _sig("tkv_store_destroy", _vp, res=None)
@@ -299,6 +300,10 @@ class Model:
             self._h = None
 
     __del__ = close
+
+    def set_attention(self, impl):
+        """0 = tcgen05 attention where supported (head_dim 128), 1 = mma.sync kernel."""
+        _check(_lib.tkv_model_set_attention(self._h, {"tc5": 0, "mma": 1}.get(impl, impl)))
 
     def weights(self, which):
         rows = self.cfg.vocab_size if (which == 0 or self.dtype != 1) else self.vocab_padded

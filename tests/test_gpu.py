@@ -191,6 +191,33 @@ def test_bf16_tensor_core_path_llama_shaped_gqa_swiglu_rms():
     _bf16_logit_check(kw, n_cases=3, ctx_len=300, q_len=70, seed=2)
 
 
+@pytest.mark.parametrize("ctx_len,q_len", [(0, 1), (0, 200), (1, 1), (127, 130), (300, 70), (1000, 257), (2500, 33)])
+def test_tcgen05_attention_matches_mma_kernel(ctx_len, q_len):
+    """head_dim 128 runs the tcgen05/TMEM attention; the mma.sync kernel (already pinned to the
+    oracle) is its reference on identical inputs, cached-prefix mode and block-mask mode."""
+    kw = dict(num_layers=1, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=512, ffn_dim=512, mlp="swiglu",
+              norm="rms")
+    m = N.Model(dtype="bf16", **kw)
+    rng = np.random.default_rng(ctx_len * 1000 + q_len)
+    toks = rng.integers(0, 512, q_len).tolist()
+    ck = f32_to_bf16_bits(rng.standard_normal((1, ctx_len, 256)))
+    cv = f32_to_bf16_bits(rng.standard_normal((1, ctx_len, 256)))
+    groups = [int(g) for g in np.repeat(np.arange(4), (q_len + 3) // 4)[:q_len]]
+    groups[-min(5, q_len):] = [-1] * min(5, q_len)
+    outs = {}
+    for impl in ("tc5", "mma"):
+        m.set_attention(impl)
+        a = m.forward(toks, mode=0, ctx_k=ck if ctx_len else None, ctx_v=cv if ctx_len else None)
+        b = m.forward(toks, groups=groups, mode=1)
+        outs[impl] = (a, b)
+    for i in range(2):
+        ha, hb = outs["tc5"][i]["hidden"], outs["mma"][i]["hidden"]
+        assert np.isfinite(ha).all()
+        assert np.abs(ha - hb).max() <= 3e-2 * max(1.0, np.abs(hb).max()), (i, np.abs(ha - hb).max())
+        assert np.abs(outs["tc5"][i]["logits"] - outs["mma"][i]["logits"]).max() <= 3e-2
+    m.close()
+
+
 def test_bf16_tensor_core_path_head_dim_64():
     kw = dict(num_layers=1, num_heads=4, num_kv_heads=4, head_dim=64, vocab_size=256, mlp="silu", norm="ln")
     _bf16_logit_check(kw, n_cases=3, ctx_len=97, q_len=129, seed=3)
