@@ -178,18 +178,27 @@ def main():
     ap.add_argument("--copy-engine", type=int, default=0)
     ap.add_argument("--nocache-queries", type=int, default=300, help="queries in the no-cache comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--peer-fetch", type=int, default=None,
+                    help="NVLink peer KV fetch between ranks (default: on when N > 1)")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if os.environ.get("TKV_BENCH_ONE_DEVICE"):  # test hook: every rank on GPU 0 (one-GPU boxes)
+        local = 0
+    peer_on = (world > 1) if args.peer_fetch is None else bool(args.peer_fetch)
 
     import numpy as np
     import torch
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("TKV_BENCH_ONE_DEVICE"):  # NCCL refuses two ranks on one GPU
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if os.environ.get("TKV_BENCH_ONE_DEVICE") else "cuda"
     from paper_2601_08743_b200 import native as N
     from paper_2601_08743_b200 import workloads as W
 
@@ -215,12 +224,35 @@ def main():
     def my_slice(order):
         return S.rank_slice(order, rank, world)
 
+    # NVLink peer fetch: exchange pool/directory IPC blobs; peer slot i = the i-th other rank
+    peer_status = "off"
+    others = [r for r in range(world) if r != rank]
+    if peer_on and world > 1:
+        try:
+            blob = store.peer_export()
+            blobs = [None] * world
+            torch.distributed.all_gather_object(blobs, blob)
+            store.peer_attach([blobs[r] for r in others])
+            peer_status = "on"
+        except Exception as e:  # noqa: BLE001  (reported in the JSON line; serving proceeds from host)
+            peer_status = "unavailable: %s" % str(e).splitlines()[0][:200]
+        flags = [None] * world
+        torch.distributed.all_gather_object(flags, peer_status == "on")
+        if not all(flags):
+            peer_status = peer_status if peer_status != "on" else "off (a peer failed to attach)"
+
     opts = N.serve_options(rerank_on=0, pipeline_on=1, capacity=args.capacity, policy="lru", b_c=args.b_c,
-                           b_m=args.b_m, copy_engine=args.copy_engine, time_kernels=1)
+                           b_m=args.b_m, copy_engine=args.copy_engine, time_kernels=1,
+                           peer_fetch=int(peer_status == "on"))
 
     def step():
-        sl = my_slice(global_order())  # global rerank inside the step, on every rank
+        order = global_order()  # global rerank inside the step, on every rank
+        sl = my_slice(order)
         qs = [(analyzed[i]["assembly_order"], analyzed[i]["remainder"]) for i in sl]
+        if peer_status == "on":  # every peer's slice: the host-side residency prediction
+            for slot, r in enumerate(others):
+                store.peer_plan(slot, [(analyzed[i]["assembly_order"], len(analyzed[i]["remainder"]))
+                                       for i in S.rank_slice(order, r, world)])
         return store.serve(qs, opts)
 
     def barrier():
@@ -250,7 +282,7 @@ def main():
     dev_ms = sum(r["makespan_ms"] for r in results)
     total_ms = dev_ms
     if world > 1:
-        t = torch.tensor([dev_ms], device="cuda")
+        t = torch.tensor([dev_ms], device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     n_local = len(results[0]["order"])
@@ -280,7 +312,7 @@ def main():
                                                                         b_c=args.b_c, b_m=args.b_m))
     e2e_s = time.perf_counter() - te
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_h2d = e2e_res["h2d_bytes"] + e2e_res["meta_bytes"] + sum(len(x.encode()) for x in e2e_texts)
@@ -324,6 +356,10 @@ def main():
                     "frac_of_pcie": (dem_b / (dem_ms / 1e3) / 1e9) / pcie if dem_ms else None,
                     "gbs_definition": "demand-stream bytes / summed per-window spans of its back-to-back copies",
                     "copy_engine": ["dma", "sm-16B-kernel"][args.copy_engine],
+                    "peer_fetch": peer_status,
+                    "peer_routed_bytes_per_step": sum(r["peer_routed_bytes"] for r in results) / args.steps,
+                    "peer_bytes_per_step": sum(r["peer_bytes"] for r in results) / args.steps,
+                    "peer_fallback_bytes_per_step": sum(r["peer_fallback_bytes"] for r in results) / args.steps,
                     "hits_misses_swaps_prefetch": results[0]["counters"]},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",

@@ -143,6 +143,8 @@ typedef struct {
     int sm_copy_ctas;
     int nocache;       /* 1: the no-cache baseline (block-masked full prefill, same kernels) */
     int time_kernels;  /* per-GEMM CUDA events (roofline) */
+    int peer_fetch;    /* 1: misses predicted resident on an attached peer GPU are copied over NVLink */
+    int peer_ctas;     /* CTAs per peer-fetch copy */
 } tkv_serve_options;
 void tkv_serve_options_default(tkv_serve_options* o);
 
@@ -158,6 +160,25 @@ int tkv_serve_text(tkv_store* s, const tkv_engine* e, size_t n, const char* cons
                    const tkv_serve_options* o, float* logits_out, char** result_json);
 /* binds corpus token ids + group ids (needed by the no-cache baseline) */
 int tkv_store_bind_engine(tkv_store* s, const tkv_engine* e);
+
+/* ---- NVLink peer KV fetch (no reference counterpart: the reference is one
+ * process). A miss whose table is resident in a peer GPU's pool is copied from that pool over
+ * NVLink instead of from the host arena; it changes the SOURCE of a miss, never the trace.
+ * export: the opaque IPC blob of this store (pool slab + residency directory), *n = its size;
+ * dir_entries = table-id capacity of the directory (0: max arena table id + 1).
+ * attach: the blobs of the n peers (peer slot i = blobs[i]); once per store.
+ * plan: peer slot's upcoming batch (tables per query in assembly order, suffix lengths) for the
+ * host-side residency prediction that routes misses; serve() with peer_fetch = 1 uses it.
+ * publish/unpublish: hold a table resident in this store's pool and visible to peers (tests,
+ * static sharing). fetch: copy a table into fresh pages from the first peer holding it (host
+ * arena per CTA otherwise) and read the landed bytes back; *peer_bytes = bytes served by peers. */
+int tkv_store_peer_export(tkv_store* s, int dir_entries, void* blob_out, size_t cap, size_t* n);
+int tkv_store_peer_attach(tkv_store* s, int n, const void* const* blobs, const size_t* sizes);
+int tkv_store_peer_plan(tkv_store* s, int slot, size_t n, const int64_t* table_off, const int32_t* tables,
+                        const int32_t* suffix_len);
+int tkv_store_peer_publish(tkv_store* s, int table_id);
+int tkv_store_peer_unpublish(tkv_store* s, int table_id);
+int tkv_store_peer_fetch(tkv_store* s, int table_id, void* host_out, size_t bytes, uint64_t* peer_bytes);
 
 /* ---- measurement helpers ---------------------------------------------------------------- */
 /* pinned H2D copy peak over `bytes`, best of `reps` (GB/s) */

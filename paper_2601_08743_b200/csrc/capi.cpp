@@ -42,6 +42,8 @@ struct tkv_store {
     std::unique_ptr<tkv::Arena> arena;
     std::unique_ptr<tkv::PagePool> pool;
     std::unique_ptr<tkv::Server> server;
+    std::unique_ptr<tkv::PeerMesh> mesh;
+    std::unordered_map<int, std::vector<int32_t>> held;  // peer_publish: table -> pages
 };
 
 namespace {
@@ -157,6 +159,8 @@ tkv::ServeOptions serve_opts(const tkv_serve_options* o) {
     so.engine = o->copy_engine ? tkv::CopyEngine::sm : tkv::CopyEngine::dma;
     so.sm_copy_ctas = std::max(1, o->sm_copy_ctas);
     so.time_kernels = o->time_kernels != 0;
+    so.peer_fetch = o->peer_fetch != 0;
+    so.peer_ctas = std::max(1, o->peer_ctas);
     return so;
 }
 
@@ -174,6 +178,9 @@ json serve_result_json(const tkv::ServeResult& R) {
             {"meta_bytes", R.meta_bytes},
             {"copy_busy_ms", R.copy_busy_ms},
             {"h2d_demand_bytes", R.h2d_demand_bytes},
+            {"peer_routed_bytes", R.peer_routed_bytes},
+            {"peer_bytes", R.peer_bytes},
+            {"peer_fallback_bytes", R.peer_fallback_bytes},
             {"copy_demand_ms", R.copy_demand_ms},
             {"makespan_ms", R.makespan_ms},
             {"host_ms", R.host_ms},
@@ -553,6 +560,12 @@ void tkv_store_destroy(tkv_store* s) {
     if (!s) return;
     cudaSetDevice(s->model->device);
     s->server.reset();
+    for (auto& kv : s->held) {
+        if (s->mesh) tkv::launch_dir_revoke(s->mesh->local_dir(), kv.first, s->model->s);
+        s->pool->release(kv.second, s->model->s);
+    }
+    cudaStreamSynchronize(s->model->s);
+    s->mesh.reset();
     s->pool.reset();
     s->arena.reset();
     delete s;
@@ -732,6 +745,124 @@ int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, void* 
     });
 }
 
+namespace {
+tkv::PageList page_list(const std::vector<int32_t>& pages) {
+    if (pages.size() > size_t(tkv::kMaxPagesPerCopy)) throw std::invalid_argument("table spans too many pages for one copy");
+    tkv::PageList pl;
+    pl.n = int(pages.size());
+    for (size_t i = 0; i < pages.size(); ++i) pl.page[i] = pages[i];
+    return pl;
+}
+tkv::PeerMesh& mesh_of(tkv_store* s) {
+    if (!s->mesh) throw std::invalid_argument("no peer mesh: call tkv_store_peer_export first");
+    return *s->mesh;
+}
+}  // namespace
+
+int tkv_store_peer_export(tkv_store* s, int dir_entries, void* blob_out, size_t cap, size_t* n) {
+    return guard([&] {
+        need(s && n, "null argument");
+        set_device(s->model->device);
+        if (!s->mesh) {
+            const int entries = dir_entries > 0 ? dir_entries : s->arena->max_table_id() + 1;
+            need(entries > 0, "peer directory needs at least one table (load the arena first)");
+            s->mesh = std::make_unique<tkv::PeerMesh>(s->pool->base(), s->pool->page_bytes(), s->pool->n_pages(), entries);
+            s->server->set_mesh(s->mesh.get());
+        }
+        *n = sizeof(tkv::PeerBlob);
+        if (blob_out) {
+            need(cap >= sizeof(tkv::PeerBlob), "blob buffer too small");
+            const tkv::PeerBlob b = s->mesh->blob();
+            std::memcpy(blob_out, &b, sizeof(b));
+        }
+    });
+}
+
+int tkv_store_peer_attach(tkv_store* s, int n, const void* const* blobs, const size_t* sizes) {
+    return guard([&] {
+        need(s && (blobs || n == 0), "null argument");
+        set_device(s->model->device);
+        std::vector<tkv::PeerBlob> v(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            need(blobs[i] && (!sizes || sizes[i] == sizeof(tkv::PeerBlob)), "bad peer blob");
+            std::memcpy(&v[size_t(i)], blobs[i], sizeof(tkv::PeerBlob));
+        }
+        mesh_of(s).attach(v);
+    });
+}
+
+int tkv_store_peer_plan(tkv_store* s, int slot, size_t n, const int64_t* table_off, const int32_t* tables,
+                        const int32_t* suffix_len) {
+    return guard([&] {
+        need(s && table_off && (suffix_len || n == 0), "null argument");
+        need(slot >= 0 && slot < tkv::kMaxPeers, "peer slot out of range");
+        tkv::PeerPlan p;
+        for (size_t i = 0; i < n; ++i) {
+            p.tables.emplace_back(tables + table_off[i], tables + table_off[i + 1]);
+            p.suffix_len.push_back(suffix_len[i]);
+        }
+        s->server->set_peer_plan(slot, std::move(p));
+    });
+}
+
+int tkv_store_peer_publish(tkv_store* s, int table_id) {
+    return guard([&] {
+        need(s, "null argument");
+        set_device(s->model->device);
+        tkv::PeerMesh& m = mesh_of(s);
+        need(table_id >= 0 && table_id < m.dir_entries(), "table id outside the peer directory");
+        need(!s->held.count(table_id), "table already published");
+        const tkv::TableImage* img = s->arena->find(table_id);
+        if (!img) throw tablekv::Error(tablekv::Errc::unknown_table, "table " + std::to_string(table_id) + " not in the arena");
+        const size_t P = s->pool->page_bytes();
+        auto pages = s->pool->alloc(int((img->bytes + P - 1) / P));
+        tkv::copy_table_to_pages(*img, *s->pool, pages, tkv::CopyEngine::dma, 16, s->model->s);
+        tkv::launch_dir_publish(m.local_dir(), table_id, page_list(pages), s->model->s);
+        TKV_CUDA_CHECK(cudaStreamSynchronize(s->model->s));
+        s->held[table_id] = std::move(pages);
+    });
+}
+
+int tkv_store_peer_unpublish(tkv_store* s, int table_id) {
+    return guard([&] {
+        need(s, "null argument");
+        set_device(s->model->device);
+        auto it = s->held.find(table_id);
+        need(it != s->held.end(), "table not published");
+        tkv::launch_dir_revoke(mesh_of(s).local_dir(), table_id, s->model->s);
+        s->pool->release(it->second, s->model->s);
+        TKV_CUDA_CHECK(cudaStreamSynchronize(s->model->s));
+        s->held.erase(it);
+    });
+}
+
+int tkv_store_peer_fetch(tkv_store* s, int table_id, void* host_out, size_t bytes, uint64_t* peer_bytes) {
+    return guard([&] {
+        need(s && host_out, "null argument");
+        set_device(s->model->device);
+        tkv::PeerMesh& m = mesh_of(s);
+        const tkv::TableImage* img = s->arena->find(table_id);
+        if (!img) throw tablekv::Error(tablekv::Errc::unknown_table, "table " + std::to_string(table_id) + " not in the arena");
+        need(bytes == img->bytes, "byte count does not match the table image");
+        const size_t P = s->pool->page_bytes();
+        cudaStream_t st = s->model->s;
+        auto pages = s->pool->alloc(int((img->bytes + P - 1) / P));
+        tkv::PeerOrder po;
+        for (int i = 0; i < tkv::kMaxPeers; ++i) po.p[i] = int8_t(i < m.n_peers() ? i : -1);
+        TKV_CUDA_CHECK(cudaMemsetAsync(m.stats(), 0, 2 * sizeof(unsigned long long), st));
+        tkv::launch_peer_fetch(m.view(), po, table_id, img->mapped, img->bytes, s->pool->base(), P, page_list(pages),
+                               m.stats(), 64, st);
+        for (size_t i = 0; i * P < img->bytes; ++i)
+            TKV_CUDA_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + i * P, s->pool->base() + size_t(pages[i]) * P,
+                                           std::min(P, img->bytes - i * P), cudaMemcpyDeviceToHost, st));
+        unsigned long long stv[2];
+        TKV_CUDA_CHECK(cudaMemcpyAsync(stv, m.stats(), sizeof(stv), cudaMemcpyDeviceToHost, st));
+        TKV_CUDA_CHECK(cudaStreamSynchronize(st));
+        s->pool->release(pages, st);
+        if (peer_bytes) *peer_bytes = stv[0];
+    });
+}
+
 int tkv_store_info(const tkv_store* s, size_t* tables, size_t* arena_bytes, size_t* free_pages) {
     return guard([&] {
         need(s, "null argument");
@@ -757,6 +888,8 @@ void tkv_serve_options_default(tkv_serve_options* o) {
     o->switch_overhead = 5.0;
     o->copy_engine = 0;
     o->sm_copy_ctas = 16;
+    o->peer_fetch = 0;
+    o->peer_ctas = 64;
 }
 
 namespace {

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <deque>
 #include <unordered_map>
 #include <vector>
@@ -35,6 +36,11 @@ class Arena {
     const TableImage* find(int table_id) const;
     size_t total_bytes() const { return total_; }
     size_t size() const { return tables_.size(); }
+    int max_table_id() const {
+        int m = -1;
+        for (const auto& kv : tables_) m = std::max(m, kv.first);
+        return m;
+    }
 
    private:
     uint8_t* reserve(size_t bytes);

@@ -67,12 +67,69 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::vector<int>& suffix_len,
+                      const ServeOptions& opts, const Arena& arena) {
+    BatchTrace bt;
+    int n_bits = 0;
+    for (const auto& q : tables)
+        for (int t : q) n_bits = std::max(n_bits, t + 1);
+    std::vector<tablekv::QueryRecord> recs;
+    recs.reserve(tables.size());
+    for (size_t i = 0; i < tables.size(); ++i) {
+        auto r = tablekv::make_query_record("q" + std::to_string(i), {}, tables[i], std::max(1, n_bits), suffix_len[i]);
+        r.tables = tables[i];
+        recs.push_back(std::move(r));
+    }
+    bt.order = tablekv::serving_order(recs, opts.run);
+    std::vector<tablekv::SimQuery> sims;
+    for (size_t i : bt.order) sims.push_back({recs[i].query_id, tables[i], suffix_len[i]});
+    bt.plan = tablekv::schedule(std::move(sims), opts.run.b_c, opts.run.b_m);
+    auto meta = std::make_shared<MetaTier>(arena);
+    tablekv::TieredCache cache(opts.run.capacity, opts.run.policy, meta);
+    bt.trace = tablekv::build_trace(bt.plan, opts.cost, cache);
+    bt.counters = cache.counters();
+    bt.managed = opts.run.capacity > 0;
+    return bt;
+}
+
+std::unordered_map<int, std::vector<std::pair<int, int>>> residency_intervals(const BatchTrace& bt) {
+    // the executor publishes demand loads of window w at compute(w), prefetches of w at
+    // compute(w + 1), and revokes a victim after compute(w) (serve() below)
+    std::unordered_map<int, std::vector<std::pair<int, int>>> live;
+    std::unordered_map<int, int> open;  // table -> publish window
+    if (bt.plan.windows.empty() || !bt.managed) return live;
+    auto close = [&](int t, int w) {
+        auto it = open.find(t);
+        if (it == open.end()) return;
+        if (it->second <= w) live[t].push_back({it->second, w});
+        open.erase(it);
+    };
+    const int last = int(bt.trace.windows.size()) - 1;
+    for (int w = 0; w <= last; ++w) {
+        const auto& wt = bt.trace.windows[size_t(w)];
+        for (const auto& r : wt.boundary)
+            if (r.miss) close(r.evicted, w), open[r.table] = w;
+        for (const auto& r : wt.prefetch) close(r.evicted, w), open[r.table] = w + 1;
+        for (const auto& q : wt.emergency)
+            for (const auto& r : q) close(r.evicted, w), open[r.table] = w;
+    }
+    for (auto& kv : open)
+        if (kv.second <= last) live[kv.first].push_back({kv.second, last});
+    return live;
+}
+
 Server::Server(Model& model, Arena& arena, PagePool& pool) : model_(model), arena_(arena), pool_(pool) {
     int lo, hi;
     TKV_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, hi));
     TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&ds_, cudaStreamNonBlocking, hi));
     TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&ps_, cudaStreamNonBlocking, lo));
+    TKV_CUDA_CHECK(cudaStreamCreateWithPriority(&xs_, cudaStreamNonBlocking, hi));
+}
+
+void Server::set_peer_plan(int slot, PeerPlan plan) {
+    if (plan.tables.size() != plan.suffix_len.size()) throw std::invalid_argument("peer plan: tables/suffix_len size mismatch");
+    peer_plans_[slot] = std::move(plan);
 }
 
 Server::~Server() {
@@ -81,6 +138,7 @@ Server::~Server() {
     cudaStreamDestroy(cs_);
     cudaStreamDestroy(ds_);
     cudaStreamDestroy(ps_);
+    cudaStreamDestroy(xs_);
 }
 
 void Server::set_table_tokens(std::vector<std::vector<int32_t>> tt, std::vector<int> group_of) {
@@ -113,24 +171,40 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     TKV_CUDA_CHECK(cudaStreamWaitEvent(ps_, t0));
 
     // ---- host: records, rerank, schedule, canonical trace (reference decisions)
-    int n_bits = 0;
-    for (const auto& q : queries)
-        for (int t : q.tables) n_bits = std::max(n_bits, t + 1);
-    std::vector<tablekv::QueryRecord> recs;
-    recs.reserve(queries.size());
-    for (const auto& q : queries) {
-        auto r = tablekv::make_query_record(q.id, {}, q.tables, std::max(1, n_bits), int(q.suffix.size()));
-        r.tables = q.tables;
-        recs.push_back(std::move(r));
-    }
-    R.order = tablekv::serving_order(recs, opts.run);
-    std::vector<tablekv::SimQuery> sims;
-    for (size_t i : R.order) sims.push_back({queries[i].id, queries[i].tables, int(queries[i].suffix.size())});
-    const tablekv::BatchPlan plan = tablekv::schedule(std::move(sims), opts.run.b_c, opts.run.b_m);
-    auto meta = std::make_shared<MetaTier>(arena_);
-    tablekv::TieredCache cache(opts.run.capacity, opts.run.policy, meta);
-    const tablekv::Trace tr = tablekv::build_trace(plan, opts.cost, cache);
-    R.counters = cache.counters();
+    std::vector<std::vector<int>> qt;
+    std::vector<int> qn;
+    for (const auto& q : queries) qt.push_back(q.tables), qn.push_back(int(q.suffix.size()));
+    BatchTrace bt = plan_batch(qt, qn, opts, arena_);
+    R.order = std::move(bt.order);
+    const tablekv::BatchPlan& plan = bt.plan;
+    const tablekv::Trace& tr = bt.trace;
+    R.counters = bt.counters;
+    // peers' predicted residency (table -> [published window, revoked window] intervals per slot)
+    const bool peering = opts.peer_fetch && mesh_ && mesh_->n_peers() > 0;
+    std::vector<std::unordered_map<int, std::vector<std::pair<int, int>>>> peer_live;
+    if (peering)
+        for (int p = 0; p < mesh_->n_peers(); ++p) {
+            auto it = peer_plans_.find(p);
+            peer_live.push_back(it == peer_plans_.end() ? decltype(peer_live)::value_type{}
+                                                        : residency_intervals(plan_batch(it->second.tables, it->second.suffix_len, opts, arena_)));
+        }
+    // the peers whose pool should hold table t while this GPU is around window w (one window of
+    // slack either side for skew between ranks); -1 terminated
+    auto predict = [&](int t, int w) {
+        PeerOrder o;
+        for (int i = 0; i < kMaxPeers; ++i) o.p[i] = -1;
+        int k = 0;
+        for (size_t p = 0; p < peer_live.size() && k < kMaxPeers; ++p) {
+            auto it = peer_live[p].find(t);
+            if (it == peer_live[p].end()) continue;
+            for (const auto& iv : it->second)
+                if (iv.first <= w - 2 && iv.second >= w) {
+                    o.p[k++] = int8_t(p);
+                    break;
+                }
+        }
+        return o;
+    };
 
     // ---- sizing: context slab for the largest window, rope table for the longest row
     long max_ctx_rows = 0;
@@ -160,8 +234,8 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     if (opts.keep_logits) logits_host.resize(queries.size() * size_t(vp));
 
     // ---- physical replay
-    std::unordered_map<int, std::vector<int32_t>> resident;
     const bool managed = opts.run.capacity > 0;
+    std::unordered_map<int, std::vector<int32_t>> resident;
     // Bookkeeping first, bytes second: records only allocate pages and queue the copy; each
     // window's copies are then issued back-to-back per stream so the copy engines stream
     // without host-side gaps between tables.
@@ -169,20 +243,53 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         const TableImage* img;
         std::vector<int32_t> pages;
         cudaStream_t st;
+        PeerOrder peers;
     };
     std::vector<PendingCopy> pending;
+    size_t cur_window = 0;
     auto load = [&](int t, cudaStream_t st) {
         const TableImage* img = arena_.find(t);
         std::vector<int32_t> pages = pool_.alloc(int((img->bytes + P - 1) / P));
-        pending.push_back({img, pages, st});
-        R.h2d_bytes += img->bytes;
-        if (st == ds_) R.h2d_demand_bytes += img->bytes;
+        PeerOrder po{};
+        for (int i = 0; i < kMaxPeers; ++i) po.p[i] = -1;
+        if (peering && managed && img->bytes % 16 == 0 && int(pages.size()) <= kMaxPagesPerCopy) po = predict(t, int(cur_window));
+        if (po.p[0] >= 0) {
+            pending.push_back({img, pages, xs_, po});
+            R.peer_routed_bytes += img->bytes;
+        } else {
+            pending.push_back({img, pages, st, po});
+            R.h2d_bytes += img->bytes;
+            if (st == ds_) R.h2d_demand_bytes += img->bytes;
+        }
         return pages;
     };
-    auto flush_copies = [&](cudaStream_t st) {
-        for (const auto& c : pending)
-            if (c.st == st) copy_table_to_pages(*c.img, pool_, c.pages, opts.engine, opts.sm_copy_ctas, st);
+    auto page_list = [](const std::vector<int32_t>& pages) {
+        PageList pl;
+        pl.n = int(pages.size());
+        for (size_t i = 0; i < pages.size(); ++i) pl.page[i] = pages[i];
+        return pl;
     };
+    auto flush_copies = [&](cudaStream_t st) {
+        for (const auto& c : pending) {
+            if (c.st != st) continue;
+            if (st == xs_)
+                launch_peer_fetch(mesh_->view(), c.peers, c.img->table_id, c.img->mapped, c.img->bytes, pool_.base(), P,
+                                  page_list(c.pages), mesh_->stats(), opts.peer_ctas, xs_);
+            else
+                copy_table_to_pages(*c.img, pool_, c.pages, opts.engine, opts.sm_copy_ctas, st);
+        }
+    };
+    // tables this GPU has published in its directory for peers (table -> pages), and the loads
+    // waiting to be published: demand loads of window w at compute(w), prefetches at compute(w+1)
+    std::unordered_map<int, std::vector<int32_t>> published;
+    std::vector<std::pair<int, std::vector<int32_t>>> pub_now, pub_next;
+    const bool sharing = mesh_ != nullptr && managed;
+    if (peering) {
+        TKV_CUDA_CHECK(cudaMemsetAsync(mesh_->stats(), 0, 2 * sizeof(unsigned long long), cs_));
+        cudaEvent_t z = evp.get();
+        TKV_CUDA_CHECK(cudaEventRecord(z, cs_));
+        TKV_CUDA_CHECK(cudaStreamWaitEvent(xs_, z));
+    }
     std::vector<cudaEvent_t> win_end(plan.windows.size());
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dspan, pspan;
     cudaEvent_t prev_pref = nullptr;
@@ -192,7 +299,10 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
         const auto& w = plan.windows[wi];
         const auto& wt = tr.windows[wi];
-        std::vector<std::vector<int32_t>> dropped;  // evicted this window: recycle after compute(wi)
+        std::vector<std::pair<int, std::vector<int32_t>>> dropped;  // evicted this window: recycle after compute(wi)
+        cur_window = wi;
+        pub_now.swap(pub_next);  // prefetches of the previous window
+        pub_next.clear();
         // Pages of tables evicted during this window stay readable until compute(wi) is done.
         // The reference trace lets a query's own emergency get evict another of its tables
         // without reloading it (pipeline.cpp:98-107), so snapshots may need them.
@@ -202,7 +312,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             auto it = resident.find(victim);
             if (it != resident.end()) {
                 gone[victim] = it->second;
-                dropped.push_back(std::move(it->second));
+                dropped.push_back({victim, std::move(it->second)});
                 resident.erase(it);
             }
         };
@@ -212,12 +322,14 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             if (!r.miss) continue;
             evict(r.evicted);
             resident[r.table] = load(r.table, ds_);
+            if (sharing) pub_now.push_back({r.table, resident[r.table]});
             R.trace.back().bytes = arena_.find(r.table)->bytes;
         }
         for (const auto& r : wt.prefetch) {
             R.trace.push_back({int(wi), 1, -1, r.table, r.evicted, true, arena_.find(r.table)->bytes});
             evict(r.evicted);
             resident[r.table] = load(r.table, ps_);
+            if (sharing) pub_next.push_back({r.table, resident[r.table]});
         }
         // per query: emergency reloads, then a snapshot of its tables' pages
         struct Seg {
@@ -231,8 +343,10 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 R.trace.push_back({int(wi), 2, long(qi), r.table, r.evicted, true, arena_.find(r.table)->bytes});
                 evict(r.evicted);
                 auto pages = load(r.table, ds_);
-                if (managed)
+                if (managed) {
+                    if (sharing) pub_now.push_back({r.table, pages});
                     resident[r.table] = std::move(pages);
+                }
                 else
                     local[r.table] = std::move(pages);
             }
@@ -244,7 +358,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 qsegs[qi - w.begin].push_back({t, arena_.find(t)->tokens, *pg});
             }
             if (!managed)
-                for (auto& kv : local) dropped.push_back(std::move(kv.second));
+                for (auto& kv : local) dropped.push_back({-1, std::move(kv.second)});
         }
         cudaEvent_t d0 = evp.get(), p0 = evp.get(), d1 = evp.get(), p1 = evp.get();
         TKV_CUDA_CHECK(cudaEventRecord(d0, ds_));
@@ -255,11 +369,29 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         TKV_CUDA_CHECK(cudaEventRecord(p1, ps_));
         dspan.push_back({d0, d1});
         pspan.push_back({p0, p1});
+        cudaEvent_t x1 = nullptr;
+        if (peering) {
+            // peer copies of window w run during compute(w-1): the peers are then around the
+            // same window, where the prediction placed the table
+            if (wi >= 2) TKV_CUDA_CHECK(cudaStreamWaitEvent(xs_, win_end[wi - 2]));
+            flush_copies(xs_);
+            x1 = evp.get();
+            TKV_CUDA_CHECK(cudaEventRecord(x1, xs_));
+        }
 
         // ---- compute(wi): needs this window's demand loads and every earlier prefetch
         TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, d1));
         if (prev_pref) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, prev_pref));
         prev_pref = p1;
+        if (x1) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, x1));
+        // publish what landed for this window (still resident with the same pages)
+        for (auto& [t, pages] : pub_now) {
+            auto it = resident.find(t);
+            if (it == resident.end() || it->second != pages) continue;
+            launch_dir_publish(mesh_->local_dir(), t, page_list(pages), cs_);
+            published[t] = pages;
+        }
+        pub_now.clear();
 
         std::vector<GatherSeg> segs;
         std::vector<int32_t> page_ids, tokens, pos, logit_rows;
@@ -349,17 +481,33 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         }
         win_end[wi] = evp.get();
         TKV_CUDA_CHECK(cudaEventRecord(win_end[wi], cs_));
-        for (auto& pg : dropped) pool_.release(pg, cs_);
+        for (auto& [t, pg] : dropped) {
+            auto it = t >= 0 ? published.find(t) : published.end();
+            if (it != published.end() && it->second == pg) {  // peers must drain before the pages recycle
+                launch_dir_revoke(mesh_->local_dir(), t, cs_);
+                published.erase(it);
+            }
+            pool_.release(pg, cs_);
+        }
         // the k-th prefilling query of this window writes its argmax to d_argmax[w.begin + k]
         for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(w.begin + k);  // slot, resolved below
     }
     // the batch's cache dies with it: every still-resident table's pages go back to the pool
+    for (auto& kv : published) launch_dir_revoke(mesh_->local_dir(), kv.first, cs_);
+    published.clear();
     for (auto& kv : resident) pool_.release(kv.second, cs_);
     resident.clear();
     R.host_ms = now_ms() - host0;
     TKV_CUDA_CHECK(cudaStreamSynchronize(ps_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(ds_));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(xs_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+    if (peering) {
+        unsigned long long st[2];
+        TKV_CUDA_CHECK(cudaMemcpy(st, mesh_->stats(), sizeof(st), cudaMemcpyDeviceToHost));
+        R.peer_bytes = st[0];
+        R.peer_fallback_bytes = st[1];
+    }
     std::vector<int32_t> am(queries.size());
     TKV_CUDA_CHECK(cudaMemcpy(am.data(), d_argmax, sizeof(int32_t) * queries.size(), cudaMemcpyDeviceToHost));
     for (auto& a : R.argmax)

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "model.cuh"
+#include "peer.cuh"
 #include "runtime.cuh"
 #include "tablekv/pipeline.hpp"
 
@@ -29,6 +30,16 @@ struct ServeOptions {
     int sm_copy_ctas = 16;
     bool keep_logits = false;      // copy first-token logits back (parity tests)
     bool time_kernels = false;     // per-GEMM events (bench roofline)
+    bool peer_fetch = false;       // misses predicted resident on an attached peer come over NVLink
+    int peer_ctas = 64;            // CTAs per peer-fetch copy
+};
+
+// A peer's upcoming batch, as it will serve it (its queries' tables; same run options). Every
+// rank's trace is deterministic, so replaying it here predicts in which of the peer's windows a
+// table is resident — the host-side residency directory that routes a miss to the peer.
+struct PeerPlan {
+    std::vector<std::vector<int>> tables;
+    std::vector<int> suffix_len;
 };
 
 struct TraceEvent {  // one cache decision that moved bytes (or a boundary hit)
@@ -50,6 +61,8 @@ struct ServeResult {
     tablekv::CacheCounters counters;
     size_t h2d_bytes = 0, meta_bytes = 0;
     size_t h2d_demand_bytes = 0;           // boundary + emergency loads (demand copy stream)
+    size_t peer_routed_bytes = 0;          // misses routed to the NVLink peer-fetch path
+    unsigned long long peer_bytes = 0, peer_fallback_bytes = 0;  // ... served by a peer / by the host arena
     double copy_busy_ms = 0;               // sum of per-window copy spans (both copy streams)
     double copy_demand_ms = 0;             // demand stream only (its copies run back to back)
     double makespan_ms = 0, host_ms = 0;
@@ -59,6 +72,19 @@ struct ServeResult {
     double attn_ms = 0;
     long total_ctx_tokens = 0, total_suffix_tokens = 0;
 };
+
+// host half of the executor: rerank -> schedule -> canonical trace over a metadata-only tier
+struct BatchTrace {
+    std::vector<size_t> order;
+    tablekv::BatchPlan plan;
+    tablekv::Trace trace;
+    tablekv::CacheCounters counters;
+    bool managed = true;
+};
+BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::vector<int>& suffix_len,
+                      const ServeOptions& opts, const Arena& arena);
+// table -> [first, last] windows during which the executor keeps it published for peers
+std::unordered_map<int, std::vector<std::pair<int, int>>> residency_intervals(const BatchTrace& bt);
 
 class Server {
    public:
@@ -70,6 +96,9 @@ class Server {
     // baseline: full block-masked prefill of [tables ; suffix] per query, no cache, same windows
     ServeResult serve_nocache(const std::vector<ServeQuery>& queries, const ServeOptions& opts);
     cudaStream_t compute_stream() const { return cs_; }
+    // NVLink peer fetch: the mesh (owned by the store) and the peers' upcoming batches
+    void set_mesh(PeerMesh* m) { mesh_ = m; }
+    void set_peer_plan(int slot, PeerPlan plan);
 
    private:
     void ensure_ctx(size_t bytes);
@@ -77,6 +106,9 @@ class Server {
     Arena& arena_;
     PagePool& pool_;
     cudaStream_t cs_ = nullptr, ds_ = nullptr, ps_ = nullptr;  // compute, demand copies, prefetch copies
+    cudaStream_t xs_ = nullptr;                                 // peer (NVLink) copies
+    PeerMesh* mesh_ = nullptr;
+    std::unordered_map<int, PeerPlan> peer_plans_;
     void* ctx_buf_ = nullptr;
     size_t ctx_cap_ = 0;
     std::vector<std::vector<int32_t>> table_tokens_;

@@ -45,7 +45,8 @@ class tkv_serve_options(C.Structure):
     _fields_ = [("rerank_on", C.c_int), ("pipeline_on", C.c_int), ("capacity", C.c_size_t), ("policy", C.c_int),
                 ("b_c", C.c_int), ("b_m", C.c_int), ("seed", C.c_uint64), ("fixed_anchor", C.c_int),
                 ("compute_per_token", C.c_double), ("load_per_token", C.c_double), ("switch_overhead", C.c_double),
-                ("copy_engine", C.c_int), ("sm_copy_ctas", C.c_int), ("nocache", C.c_int), ("time_kernels", C.c_int)]
+                ("copy_engine", C.c_int), ("sm_copy_ctas", C.c_int), ("nocache", C.c_int), ("time_kernels", C.c_int),
+                ("peer_fetch", C.c_int), ("peer_ctas", C.c_int)]
 
 
 def _sig(name, *args, res=C.c_int):
@@ -94,6 +95,12 @@ _sig("tkv_store_assemble", _vp, _i32p, C.c_int, _vp, _vp, C.POINTER(C.c_int))
 _sig("tkv_store_info", _vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
 _sig("tkv_store_bind_engine", _vp, _vp)
 _sig("tkv_serve_options_default", C.POINTER(tkv_serve_options), res=None)
+_sig("tkv_store_peer_export", _vp, C.c_int, _vp, C.c_size_t, C.POINTER(C.c_size_t))
+_sig("tkv_store_peer_attach", _vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_size_t))
+_sig("tkv_store_peer_plan", _vp, C.c_int, C.c_size_t, _i64p, _i32p, _i32p)
+_sig("tkv_store_peer_publish", _vp, C.c_int)
+_sig("tkv_store_peer_unpublish", _vp, C.c_int)
+_sig("tkv_store_peer_fetch", _vp, C.c_int, _vp, C.c_size_t, _u64p)
 _sig("tkv_serve", _vp, C.c_size_t, _i64p, _i32p, _i64p, _i32p, C.POINTER(tkv_serve_options), _fp, C.POINTER(_vp))
 _sig("tkv_serve_text", _vp, _vp, C.c_size_t, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
      C.POINTER(tkv_serve_options), _fp, C.POINTER(_vp))
@@ -422,6 +429,45 @@ class Store:
         if want_logits:
             r["logits"] = logits[:, :self.model.cfg.vocab_size]
         return r
+
+    # ---- NVLink peer KV fetch
+    def peer_export(self, dir_entries=0) -> bytes:
+        """This store's IPC blob (pool slab + residency directory) for the other ranks."""
+        n = C.c_size_t()
+        _check(_lib.tkv_store_peer_export(self._h, dir_entries, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(_lib.tkv_store_peer_export(self._h, dir_entries, C.cast(buf, _vp), n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def peer_attach(self, blobs):
+        """blobs: the other ranks' peer_export() bytes; peer slot i = blobs[i]."""
+        bufs = [C.create_string_buffer(b, len(b)) for b in blobs]
+        arr = (_vp * max(1, len(bufs)))(*[C.cast(b, _vp) for b in bufs])
+        sizes = (C.c_size_t * max(1, len(bufs)))(*[len(b) for b in blobs])
+        _check(_lib.tkv_store_peer_attach(self._h, len(bufs), arr, sizes))
+
+    def peer_plan(self, slot, queries):
+        """queries: the peer's upcoming batch as (tables, suffix or suffix length) pairs."""
+        toff = np.zeros(len(queries) + 1, np.int64)
+        for i, (ts, _) in enumerate(queries):
+            toff[i + 1] = toff[i] + len(ts)
+        tabs = _arr([t for ts, _ in queries for t in ts] or [0], np.int32)
+        sl = _arr([sx if isinstance(sx, int) else len(sx) for _, sx in queries] or [0], np.int32)
+        _check(_lib.tkv_store_peer_plan(self._h, slot, len(queries), _ptr(toff, C.c_int64), _ptr(tabs, C.c_int32),
+                                        _ptr(sl, C.c_int32)))
+
+    def peer_publish(self, table_id):
+        _check(_lib.tkv_store_peer_publish(self._h, table_id))
+
+    def peer_unpublish(self, table_id):
+        _check(_lib.tkv_store_peer_unpublish(self._h, table_id))
+
+    def peer_fetch(self, table_id, nbytes):
+        """(landed bytes, bytes that came from a peer)"""
+        out = np.zeros(nbytes, np.uint8)
+        pb = C.c_uint64()
+        _check(_lib.tkv_store_peer_fetch(self._h, table_id, out.ctypes.data, nbytes, C.byref(pb)))
+        return out, pb.value
 
     def serve_text(self, engine: Engine, texts, ids=None, options=None, want_logits=False, **kw):
         o = options or serve_options(**kw)
