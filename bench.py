@@ -325,6 +325,8 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+    tpath = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     achieved_tf = gemm_fl / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -363,7 +365,8 @@ def main():
                     "hits_misses_swaps_prefetch": results[0]["counters"]},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": None,
+                     "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": traffic.get("dram_bytes_per_launch"),
+                     "traffic_source": traffic.get("source"), "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "share_of_step": gemm_ms / dev_ms if dev_ms else None},
         "gather": {"ms_per_step": sum(r["gather_ms"] for r in results) / args.steps},

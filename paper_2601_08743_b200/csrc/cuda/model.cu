@@ -3,6 +3,7 @@
 //     tensor-core attention over [cached prefix ; own rows], f32 residual stream.
 //   f32 / f64 (reference-precision path): the SIMT kernels of simt.cu, operation-for-operation
 //     the reference's arithmetic (attention.hpp:210-247 and :368-414).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -242,6 +243,14 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
     for (int si = 0; si < a.n_seqs; ++si)
         for (int t0 = 0; t0 < a.seqs_host[si].n_own; t0 += tq)
             for (int kh = 0; kh < c.kv_heads; ++kh) tiles.push_back(make_int4(si, t0, kh, 0));
+    if (use_tc5)  // persistent kernel walks the list round-robin: heaviest items first balances the SMs
+        std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& x, const int4& y) {
+            auto cost = [&](const int4& w) {
+                const AttnSeq& q = a.seqs_host[w.x];
+                return (q.n_ctx + 63) / 64 + (std::min(q.n_own, w.y + tq) + 63) / 64;
+            };
+            return cost(x) > cost(y);
+        });
     const int4* d_tiles = tiles.empty() ? nullptr
                                         : static_cast<const int4*>(ring_.upload(tiles.data(), tiles.size() * sizeof(int4), s));
     long nl = 0;

@@ -191,7 +191,8 @@ def test_bf16_tensor_core_path_llama_shaped_gqa_swiglu_rms():
     _bf16_logit_check(kw, n_cases=3, ctx_len=300, q_len=70, seed=2)
 
 
-@pytest.mark.parametrize("ctx_len,q_len", [(0, 1), (0, 200), (1, 1), (127, 130), (300, 70), (1000, 257), (2500, 33)])
+@pytest.mark.parametrize("ctx_len,q_len", [(0, 1), (0, 200), (1, 1), (127, 130), (300, 70), (1000, 257), (2500, 33),
+                                         (200, 5000), (3000, 1200)])
 def test_tcgen05_attention_matches_mma_kernel(ctx_len, q_len):
     """head_dim 128 runs the tcgen05/TMEM attention; the mma.sync kernel (already pinned to the
     oracle) is its reference on identical inputs, cached-prefix mode and block-mask mode."""
