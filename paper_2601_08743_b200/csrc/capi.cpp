@@ -10,6 +10,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 
 #include <json.hpp>
 
@@ -926,12 +927,29 @@ int tkv_serve_text(tkv_store* s, const tkv_engine* e, size_t n, const char* cons
     std::vector<tkv::ServeQuery> qs(n);
     const int rc = guard([&] {
         need(e && texts, "null argument");
-        for (size_t i = 0; i < n; ++i) {
-            auto a = tablekv::analyze_query(e->e, ids ? ids[i] : std::to_string(i), texts[i]);
-            qs[i].id = a.record.query_id;
-            qs[i].tables = tablekv::assembly_order(e->e, a.match_order);
-            qs[i].suffix.assign(a.remainder.begin(), a.remainder.end());
-        }
+        // prompt analysis (tokenize -> Table Trie -> assembly order) is pure per prompt and the trie
+        // is immutable after construction (trie.hpp:31-33), so prompts fan out over host threads;
+        // results land by index, identical to the sequential loop
+        const size_t n_thr = std::max<size_t>(1, std::min<size_t>({n / 32 + 1, 16, std::thread::hardware_concurrency()}));
+        std::vector<std::exception_ptr> errs(n_thr);
+        auto work = [&](size_t w) {
+            try {
+                for (size_t i = w; i < n; i += n_thr) {
+                    auto a = tablekv::analyze_query(e->e, ids ? ids[i] : std::to_string(i), texts[i]);
+                    qs[i].id = a.record.query_id;
+                    qs[i].tables = tablekv::assembly_order(e->e, a.match_order);
+                    qs[i].suffix.assign(a.remainder.begin(), a.remainder.end());
+                }
+            } catch (...) {
+                errs[w] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (size_t w = 1; w < n_thr; ++w) pool.emplace_back(work, w);
+        work(0);
+        for (auto& t : pool) t.join();
+        for (auto& ep : errs)
+            if (ep) std::rethrow_exception(ep);
     });
     if (rc != TKV_OK) return rc;
     return serve_impl(s, qs, o, logits_out, result_json);

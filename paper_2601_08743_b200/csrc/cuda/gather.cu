@@ -52,7 +52,7 @@ __global__ void gather_rope_kernel(const uint8_t* __restrict__ pool, long page_b
                                    int head_dim, DType in_dt, DType out_dt, const double* __restrict__ cos_d,
                                    const double* __restrict__ sin_d, const float* __restrict__ cos_f,
                                    const float* __restrict__ sin_f, uint8_t* __restrict__ out_k,
-                                   uint8_t* __restrict__ out_v, long out_rows) {
+                                   uint8_t* __restrict__ out_v, long out_rows, int l0, int nl) {
     const int warps = blockDim.x >> 5;
     const int row = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -73,9 +73,9 @@ __global__ void gather_rope_kernel(const uint8_t* __restrict__ pool, long page_b
     const bool exact = (in_dt == DType::f32 && out_dt == DType::f32 && cos_d != nullptr);
     for (int kv = 0; kv < 2; ++kv) {
         uint8_t* out = kv == 0 ? out_k : out_v;
-        for (int l = 0; l < L; ++l) {
+        for (int l = l0; l < l0 + nl; ++l) {
             const long base = ((long(kv) * L + l) * sg.tokens + t) * row_in;
-            uint8_t* orow = out + ((long(l) * out_rows) + row) * long(kvdim) * osz;
+            uint8_t* orow = out + ((long(l - l0) * out_rows) + row) * long(kvdim) * osz;
             for (int vi = lane; vi < nvec; vi += 32) {
                 const long off = base + long(vi) * 16;
                 const long pg = off / page_bytes;
@@ -113,13 +113,15 @@ __global__ void gather_rope_kernel(const uint8_t* __restrict__ pool, long page_b
 void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
                         int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,
                         const double* cos_d, const double* sin_d, const float* cos_f, const float* sin_f, void* out_k,
-                        void* out_v, long out_rows, cudaStream_t s) {
+                        void* out_v, long out_rows, cudaStream_t s, int l0, int nl) {
     if (total_rows <= 0 || n_segs <= 0) return;
+    if (nl < 0) nl = L - l0;
+    if (l0 < 0 || l0 + nl > L) throw std::invalid_argument("gather: layer range outside the image");
     if ((long(kvdim) * dtype_size(in_dt)) % 16) throw std::invalid_argument("gather: kv row must be a multiple of 16 bytes");
     const int warps = 8;
     gather_rope_kernel<<<ceil_div(total_rows, warps), warps * 32, 0, s>>>(
         pool, long(page_bytes), d_page_ids, d_segs, n_segs, total_rows, L, kvdim, head_dim, in_dt, out_dt, cos_d, sin_d,
-        cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v), out_rows);
+        cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v), out_rows, l0, nl);
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 

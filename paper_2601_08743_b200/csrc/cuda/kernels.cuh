@@ -47,7 +47,9 @@ struct GatherSeg {
 void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
                         int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,
                         const double* cos_d, const double* sin_d, const float* cos_f, const float* sin_f,
-                        void* out_k, void* out_v, long out_rows, cudaStream_t s);
+                        void* out_k, void* out_v, long out_rows, cudaStream_t s, int l0 = 0, int nl = -1);
+// (l0, nl): gather only layers [l0, l0 + nl) of the L-layer images into out layers [0, nl) — the
+// serving path streams one layer of prefix at a time just before that layer's attention.
 
 // ---- rope tables ------------------------------------------------------------------------------
 // Host-built [max_pos][head_dim/2] tables: angle = pos * pow(base, -2k/d) in double, std::cos /

@@ -291,7 +291,25 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.q = static_cast<const __nv_bfloat16*>(q);
         aa.k_own = static_cast<const __nv_bfloat16*>(k);
         aa.v_own = static_cast<const __nv_bfloat16*>(v_l);
-        const size_t ctx_off = size_t(l) * a.ctx_rows * kvd * 2;
+        const bool streamed = a.gather_segs != nullptr;
+        if (streamed) {
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            if (timing_) {
+                e0 = timing_event();
+                e1 = timing_event();
+                TKV_CUDA_CHECK(cudaEventRecord(e0, s));
+            }
+            launch_gather_rope(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_n_segs, a.gather_rows,
+                               c.num_layers, kvd, c.head_dim, a.gather_in, DType::bf16, rope_.cos_d(), rope_.sin_d(),
+                               rope_.cos_f(), rope_.sin_f(), const_cast<void*>(a.ctx_k), const_cast<void*>(a.ctx_v),
+                               a.ctx_rows, s, l, 1);
+            ++nl;
+            if (timing_) {
+                TKV_CUDA_CHECK(cudaEventRecord(e1, s));
+                add_timed(e0, e1, -1.0);
+            }
+        }
+        const size_t ctx_off = streamed ? 0 : size_t(l) * a.ctx_rows * kvd * 2;
         aa.k_ctx = a.ctx_k ? reinterpret_cast<const __nv_bfloat16*>(static_cast<const uint8_t*>(a.ctx_k) + ctx_off) : aa.k_own;
         aa.v_ctx = a.ctx_v ? reinterpret_cast<const __nv_bfloat16*>(static_cast<const uint8_t*>(a.ctx_v) + ctx_off) : aa.v_own;
         aa.group = a.group;

@@ -76,6 +76,14 @@ struct FwdArgs {
     const void* ctx_k = nullptr;        // [L][ctx_rows][kv_dim] rotated cached keys (model dtype)
     const void* ctx_v = nullptr;
     long ctx_rows = 0;
+    // Layer-streamed prefix (bf16 path): when gather_segs is set, ctx_k / ctx_v hold ONE layer and
+    // layer l's prefix is gathered (+RoPE) from the pool pages right before layer l's attention.
+    const uint8_t* gather_pool = nullptr;
+    size_t gather_page_bytes = 0;
+    const int32_t* gather_pages = nullptr;  // device
+    const GatherSeg* gather_segs = nullptr; // device
+    int gather_n_segs = 0, gather_rows = 0;
+    DType gather_in = DType::bf16;
     void* kraw_out = nullptr;           // optional [L][M][kv_dim] pre-rotation keys (offline encode)
     void* v_out = nullptr;              // optional [L][M][kv_dim]
     void* krot_out = nullptr;           // optional [L][M][kv_dim] rotated own keys (prefill's k_rot)

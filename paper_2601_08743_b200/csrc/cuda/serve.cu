@@ -220,9 +220,13 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         max_ctx_rows = std::max(max_ctx_rows, rows);
     }
     model_.rope().ensure(max_pos);
-    ensure_ctx(std::max<size_t>(256, size_t(2) * L * size_t(max_ctx_rows) * kvd * oes));
+    // bf16 serving streams the prefix one layer at a time (gathered right before that layer's
+    // attention), so the slab holds one layer of the window's prefix, not L
+    const bool stream_ctx = mc.dtype == DType::bf16;
+    const int slab_layers = stream_ctx ? 1 : L;
+    ensure_ctx(std::max<size_t>(256, size_t(2) * slab_layers * size_t(max_ctx_rows) * kvd * oes));
     uint8_t* ctx_k = static_cast<uint8_t*>(ctx_buf_);
-    uint8_t* ctx_v = ctx_k + size_t(L) * size_t(max_ctx_rows) * kvd * oes;
+    uint8_t* ctx_v = ctx_k + size_t(slab_layers) * size_t(max_ctx_rows) * kvd * oes;
     int32_t* d_argmax = nullptr;
     float* d_logits = nullptr;
     const int vp = mc.vocab_padded();
@@ -424,7 +428,20 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         }
         R.total_suffix_tokens += M;
         StagingRing& ring = model_.ring();
-        if (ctx_rows > 0) {
+        const GatherSeg* d_segs_s = nullptr;
+        const int32_t* d_pages_s = nullptr;
+        DType in_dt_s = DType::bf16;
+        if (ctx_rows > 0 && stream_ctx && M > 0) {
+            d_segs_s = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
+            d_pages_s = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
+            R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
+            for (const auto& qs : qsegs)
+                if (!qs.empty()) {
+                    in_dt_s = arena_.find(qs.front().table)->dtype;
+                    break;
+                }
+            if (opts.time_kernels) R.gather_bytes += double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt_s) + oes);
+        } else if (ctx_rows > 0 && !stream_ctx) {
             auto* d_segs = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
             auto* d_pages = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
             R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
@@ -463,6 +480,15 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             fa.ctx_k = ctx_k;
             fa.ctx_v = ctx_v;
             fa.ctx_rows = max_ctx_rows;
+            if (d_segs_s) {
+                fa.gather_pool = pool_.base();
+                fa.gather_page_bytes = P;
+                fa.gather_pages = d_pages_s;
+                fa.gather_segs = d_segs_s;
+                fa.gather_n_segs = int(segs.size());
+                fa.gather_rows = ctx_rows;
+                fa.gather_in = in_dt_s;
+            }
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
             fa.logit_rows_host = logit_rows.data();
             fa.n_logit_rows = int(logit_rows.size());
@@ -566,71 +592,87 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
     R.window_of.assign(n, 0);
     R.argmax.assign(n, -1);
     std::vector<cudaEvent_t> win_end;
+    // Each window is prefilled in sub-batches of at most kMaxRows prompt rows (bounded activation
+    // workspace); a query's first token is ready when its sub-batch ends.
+    constexpr long kMaxRows = 65536;
+    std::vector<cudaEvent_t> sub_end;
+    std::vector<int> sub_of(n, -1);
     for (size_t b = 0, wi = 0; b < n; b += bc, ++wi) {
         const size_t e = std::min(n, b + bc);
-        std::vector<int32_t> tokens, pos, group, logit_rows;
-        std::vector<int64_t> pos64;
-        std::vector<AttnSeq> seqs;
-        std::vector<size_t> seq_query;
-        int M = 0;
-        for (size_t qi = b; qi < e; ++qi) {
-            const ServeQuery& q = queries[R.order[qi]];
-            R.window_of[qi] = int(wi);
-            if (q.suffix.empty()) continue;
-            const int row0 = M;
-            int p = 0;
-            for (int t : q.tables) {
-                for (int32_t tok : table_tokens_[size_t(t)]) {
+        size_t slot = b;  // argmax slots of this window's prefilling queries: b, b + 1, ...
+        for (size_t qb = b; qb < e;) {
+            std::vector<int32_t> tokens, pos, group, logit_rows;
+            std::vector<int64_t> pos64;
+            std::vector<AttnSeq> seqs;
+            std::vector<size_t> seq_query;
+            int M = 0;
+            size_t qi = qb;
+            for (; qi < e; ++qi) {
+                const ServeQuery& q = queries[R.order[qi]];
+                long len = long(q.suffix.size());
+                for (int t : q.tables) len += long(table_tokens_[size_t(t)].size());
+                if (M > 0 && M + len > kMaxRows) break;
+                R.window_of[qi] = int(wi);
+                sub_of[qi] = int(sub_end.size());
+                if (q.suffix.empty()) continue;
+                const int row0 = M;
+                int p = 0;
+                for (int t : q.tables) {
+                    for (int32_t tok : table_tokens_[size_t(t)]) {
+                        tokens.push_back(tok);
+                        group.push_back(group_of_[size_t(t)]);
+                        pos.push_back(p);
+                        pos64.push_back(p++);
+                    }
+                }
+                R.total_ctx_tokens += p;
+                for (int32_t tok : q.suffix) {
                     tokens.push_back(tok);
-                    group.push_back(group_of_[size_t(t)]);
+                    group.push_back(-1);
                     pos.push_back(p);
                     pos64.push_back(p++);
                 }
+                M += p;
+                seqs.push_back({row0, p, 0, 0});
+                seq_query.push_back(qi);
+                logit_rows.push_back(M - 1);
             }
-            R.total_ctx_tokens += p;
-            for (int32_t tok : q.suffix) {
-                tokens.push_back(tok);
-                group.push_back(-1);
-                pos.push_back(p);
-                pos64.push_back(p++);
+            qb = qi;
+            R.total_suffix_tokens += M;
+            if (M > 0) {
+                StagingRing& ring = model_.ring();
+                FwdArgs fa;
+                fa.M = M;
+                fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
+                fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
+                fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
+                fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
+                fa.n_seqs = int(seqs.size());
+                fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
+                fa.seqs_host = seqs.data();
+                fa.mode = 1;
+                fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+                fa.logit_rows_host = logit_rows.data();
+                fa.n_logit_rows = int(logit_rows.size());
+                fa.logits_out = d_logits;
+                fa.argmax_out = d_argmax + slot;
+                R.meta_bytes += tokens.size() * 20 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
+                model_.set_timing(opts.time_kernels);
+                model_.forward(fa, cs_);
+                R.launches += model_.launches();
+                if (opts.keep_logits) {
+                    for (size_t k = 0; k < seq_query.size(); ++k)
+                        TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
+                                                       sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
+                    TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+                }
+                for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(slot + k);
+                slot += seq_query.size();
             }
-            M += p;
-            seqs.push_back({row0, p, 0, 0});
-            seq_query.push_back(qi);
-            logit_rows.push_back(M - 1);
+            sub_end.push_back(evp.get());
+            TKV_CUDA_CHECK(cudaEventRecord(sub_end.back(), cs_));
         }
-        R.total_suffix_tokens += M;
-        if (M > 0) {
-            StagingRing& ring = model_.ring();
-            FwdArgs fa;
-            fa.M = M;
-            fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
-            fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
-            fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
-            fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
-            fa.n_seqs = int(seqs.size());
-            fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
-            fa.seqs_host = seqs.data();
-            fa.mode = 1;
-            fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
-            fa.logit_rows_host = logit_rows.data();
-            fa.n_logit_rows = int(logit_rows.size());
-            fa.logits_out = d_logits;
-            fa.argmax_out = d_argmax + b;
-            R.meta_bytes += tokens.size() * 20 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
-            model_.set_timing(opts.time_kernels);
-            model_.forward(fa, cs_);
-            R.launches += model_.launches();
-            if (opts.keep_logits) {
-                for (size_t k = 0; k < seq_query.size(); ++k)
-                    TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
-                                                   sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
-                TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
-            }
-            for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(b + k);
-        }
-        win_end.push_back(evp.get());
-        TKV_CUDA_CHECK(cudaEventRecord(win_end.back(), cs_));
+        win_end.push_back(sub_end.back());
     }
     R.host_ms = now_ms() - host0;
     TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
@@ -641,7 +683,7 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
     R.window_end_ms.resize(win_end.size());
     for (size_t wi = 0; wi < win_end.size(); ++wi) R.window_end_ms[wi] = elapsed(t0, win_end[wi]);
     R.ttft_ms.resize(n);
-    for (size_t qi = 0; qi < n; ++qi) R.ttft_ms[qi] = R.window_end_ms[size_t(R.window_of[qi])];
+    for (size_t qi = 0; qi < n; ++qi) R.ttft_ms[qi] = elapsed(t0, sub_end[size_t(sub_of[qi])]);
     R.makespan_ms = R.window_end_ms.back();
     if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
     if (opts.keep_logits) R.logits = std::move(logits_host);
