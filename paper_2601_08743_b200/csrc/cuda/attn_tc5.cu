@@ -3,19 +3,20 @@
 // (proj/include/tablekv/attention.hpp:129-176) for the serving path's [cached prefix ; own rows].
 //
 // Work item = (sequence, kv head, 2 x 128 query rows; rows = tokens x the G q-heads of the kv head):
-// two Q tiles share every K/V tile (FA4-style), so each prefix tile is read once per 2·128/G tokens
-// and the two softmax streams hide each other's latency. Persistent: one CTA per SM walks the items
-// (heaviest first); all roles keep a running K/V tile counter so rings and mbarrier phases run on
+// two Q tiles share every 128-key K/V tile and run as two softmax streams that ping-pong on the
+// tensor core (the FlashAttention-4 structure). Persistent: one CTA per SM walks the items
+// (heaviest first); every role keeps a running tile counter, so rings and mbarrier phases run on
 // from one item into the next.
-// Warp 0: TMA producer lanes (lane 0: Q pair + K tiles on a 3-deep ring, lane 16: V tiles on a
-// 2-deep ring), from the prefix slab or the own-row buffer (a tile never straddles the two).
-// Warp 1: MMA issuer — per K/V tile S_s = Q_s.K^T (s = 0, 1) into double-buffered TMEM, then
-// O_s += P_s.V for the previous tile (P_s from a double-buffered SW128 smem tile, V MN-major).
-// Warps 2-5 / 6-9: softmax of Q tile 0 / 1 — TMEM lane = query row, each thread owns a whole row
-// (64 S columns per tile), so row max / sum need no cross-warp exchange. Online softmax with
-// conditional rescale (O rescaled in TMEM only when a row max grows by more than 2^8), exp2 on the
-// MUFU with the scale folded into one FFMA. Mask: own rows see every cached prefix row + causal own
-// (query_attend, attention.hpp:368-414); the block-causal prefill mask runs on attn_tc.cu.
+// Warp 0: TMA lanes (lane 0: the item's two Q tiles + K tiles, lane 16: V tiles; 2-deep rings of
+// 32 KB tiles) from the prefix slab or the own-row buffer (a tile never straddles the two).
+// Warp 1: MMA issuer, order PV_0(t) QK_0(t+1) PV_1(t) QK_1(t+1): S_s = Q_s.K^T (SS) into TMEM, then
+// O_s += P_s.V with P_s read from TMEM (TS: the A operand stays in tensor memory, so P never
+// touches shared memory and each PV reads only V from smem).
+// Warpgroups 1 / 2 (warps 4-7 / 8-11, registers raised with setmaxnreg): softmax of stream 0 / 1 — TMEM lane = query row, each thread owns one row:
+// loads its 128 S values, row max, conditional rescale of O in TMEM (only when the max grows by
+// more than 2^8), P = exp2(S*scale*log2e - m) packed to bf16 and stored over S's columns.
+// Mask: own rows see every cached prefix row + causal own (query_attend, attention.hpp:368-414);
+// the block-causal prefill mask runs on attn_tc.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,23 +33,21 @@ namespace tkv {
 
 namespace {
 
-constexpr int BM = 128, BN = 64, D = 128;
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 softmax Q0, warps 6-9 softmax Q1
-constexpr int kKStages = 3, kVStages = 2;
+constexpr int BM = 128, BN = 128, D = 128;
+constexpr int kThreads = 384;  // warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); warpgroups 1 / 2: softmax of Q0 / Q1
+constexpr int kKStages = 2, kVStages = 2;
 constexpr int kQHalf = BM * 64 * 2;        // Q tile: two [128 rows][64 dims] SW128 blocks, 16 KB each
-constexpr int kQTile = 2 * kQHalf;         // 32 KB; two tiles per item
-constexpr int kKVHalf = BN * 64 * 2;       // K/V tile: two [64 keys][64 dims] SW128 blocks, 8 KB each
-constexpr int kKVTile = 2 * kKVHalf;       // 16 KB
-constexpr int kPTile = BM * BN * 2;        // P: [128 rows][64 keys], one SW128 block, 16 KB
-// smem: Q0 Q1 | K ring | V ring | P[stream][buf] | barriers
-constexpr int kQOff = 0, kK0 = 2 * kQTile, kV0 = kK0 + kKStages * kKVTile, kP0 = kV0 + kVStages * kKVTile;
-constexpr int kBarOff = kP0 + 4 * kPTile;
-// QFULL QEMPTY KFULL[3] KEMPTY[3] VFULL[2] VEMPTY[2] then per stream s: SFULL[2] SFREE[2] PFULL[2]
-// PVDONE[2] OFREE
-constexpr int kStreamBars = 9;
-constexpr int kNumBars = 2 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars;
+constexpr int kQTile = 2 * kQHalf;         // 32 KB; one per stream
+constexpr int kKVHalf = BN * 64 * 2;       // K/V tile: two [128 keys][64 dims] SW128 blocks, 16 KB each
+constexpr int kKVTile = 2 * kKVHalf;       // 32 KB
+// smem: Q0 Q1 | K ring | V ring | barriers
+constexpr int kQOff = 0, kK0 = 2 * kQTile, kV0 = kK0 + kKStages * kKVTile;
+constexpr int kBarOff = kV0 + kVStages * kKVTile;
+// QFULL[2] QEMPTY[2] KFULL[2] KEMPTY[2] VFULL[2] VEMPTY[2] then per stream: SFULL PFULL PVDONE OFREE
+constexpr int kStreamBars = 4;
+constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
-// TMEM columns: S[s][b] at (2s + b) * 64, O[s] at 256 + 128 s
+// TMEM columns: S_s (f32, P_s as packed bf16 over its first 64 columns) at 128 s, O_s at 256 + 128 s
 constexpr int kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -108,6 +107,19 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t addr, uint32_t* r) {
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(addr));
 }
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+// D (TMEM) += A (TMEM, K-major) x B (smem descriptor)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                 "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -144,8 +156,6 @@ __host__ __device__ constexpr uint32_t idesc(bool b_mn, int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
-// byte offset of (row r, 16-byte chunk c) in SW128 storage whose 64-column blocks are `half` bytes apart
-__device__ __forceinline__ uint32_t sw_off(int r, int c, int half) { return uint32_t((c >> 3) * half + r * 128 + (((c & 7) ^ (r & 7)) << 4)); }
 
 struct Tc5Args {
     AttnArgs a;
@@ -180,17 +190,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s0 = smem_u32(sm);
     const uint32_t bars = s0 + kBarOff;
     auto bar = [&](int i) { return bars + uint32_t(i) * 8; };
-    const uint32_t b_qfull = bar(0), b_qempty = bar(1);
-    auto b_kfull = [&](int i) { return bar(2 + i); };
-    auto b_kempty = [&](int i) { return bar(2 + kKStages + i); };
-    auto b_vfull = [&](int i) { return bar(2 + 2 * kKStages + i); };
-    auto b_vempty = [&](int i) { return bar(2 + 2 * kKStages + kVStages + i); };
-    constexpr int kSB = 2 + 2 * kKStages + 2 * kVStages;
-    auto b_sfull = [&](int st, int i) { return bar(kSB + st * kStreamBars + i); };
-    auto b_sfree = [&](int st, int i) { return bar(kSB + st * kStreamBars + 2 + i); };
-    auto b_pfull = [&](int st, int i) { return bar(kSB + st * kStreamBars + 4 + i); };
-    auto b_pvdone = [&](int st, int i) { return bar(kSB + st * kStreamBars + 6 + i); };
-    auto b_ofree = [&](int st) { return bar(kSB + st * kStreamBars + 8); };
+    auto b_qfull = [&](int st) { return bar(st); };
+    auto b_qempty = [&](int st) { return bar(2 + st); };
+    auto b_kfull = [&](int i) { return bar(4 + i); };
+    auto b_kempty = [&](int i) { return bar(4 + kKStages + i); };
+    auto b_vfull = [&](int i) { return bar(4 + 2 * kKStages + i); };
+    auto b_vempty = [&](int i) { return bar(4 + 2 * kKStages + kVStages + i); };
+    constexpr int kSB = 4 + 2 * kKStages + 2 * kVStages;
+    auto b_sfull = [&](int st) { return bar(kSB + st * kStreamBars); };
+    auto b_pfull = [&](int st) { return bar(kSB + st * kStreamBars + 1); };
+    auto b_pvdone = [&](int st) { return bar(kSB + st * kStreamBars + 2); };
+    auto b_ofree = [&](int st) { return bar(kSB + st * kStreamBars + 3); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + kNumBars * 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -200,19 +210,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         TR(10, 0);
-        mbar_init(b_qfull, 1);
-        mbar_init(b_qempty, 1);
-        for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), 1), mbar_init(b_kempty(i), 1);
-        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), 1), mbar_init(b_vempty(i), 1);
         for (int st = 0; st < 2; ++st) {
-            for (int i = 0; i < 2; ++i) {
-                mbar_init(b_sfull(st, i), 1);
-                mbar_init(b_sfree(st, i), 4);
-                mbar_init(b_pfull(st, i), 4);
-                mbar_init(b_pvdone(st, i), 1);
-            }
+            mbar_init(b_qfull(st), 1);
+            mbar_init(b_qempty(st), 1);
+            mbar_init(b_sfull(st), 1);
+            mbar_init(b_pfull(st), 4);
+            mbar_init(b_pvdone(st), 1);
             mbar_init(b_ofree(st), 4);
         }
+        for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), 1), mbar_init(b_kempty(i), 1);
+        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), 1), mbar_init(b_vempty(i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -245,19 +252,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         return ctx ? it.sq.ctx_row0 + t * BN : it.sq.q_row0 + (t - it.n_ctx_tiles) * BN;
     };
 
+    // registers move to the softmax warpgroups (each thread holds a 128-column S row)
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA: the item's Q pair, then its K tiles
+        if (lane == 0) {  // ---- TMA: the item's two Q tiles, then its K tiles
             long g = 0;
             int j = 0;
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x, ++j) {
                 const Item it = item(w);
-                mbar_wait(b_qempty, (j & 1) ^ 1);
-                TR(8, j);
-                mbar_expect_tx(b_qfull, 2 * kQTile);
-                for (int st = 0; st < 2; ++st)
+                for (int st = 0; st < 2; ++st) {
+                    mbar_wait(b_qempty(st), (j & 1) ^ 1);
+                    mbar_expect_tx(b_qfull(st), kQTile);
                     for (int h = 0; h < 2; ++h)
-                        tma_3d(s0 + kQOff + st * kQTile + h * kQHalf, &mq, b_qfull, h * 64, it.kvh * G,
+                        tma_3d(s0 + kQOff + st * kQTile + h * kQHalf, &mq, b_qfull(st), h * 64, it.kvh * G,
                                it.sq.q_row0 + it.tok0 + st * TQ);
+                }
+                TR(8, j);
                 for (int t = 0; t < it.n_tiles; ++t, ++g) {
                     const int sk = int(g % kKStages);
                     mbar_wait(b_kempty(sk), int((g / kKStages) & 1) ^ 1);
@@ -288,62 +299,84 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             const uint32_t id_qk = idesc(false, BN), id_pv = idesc(true, D);
-            auto pv = [&](long gi, bool first) {
-                const int b = int(gi & 1), sv = int(gi % kVStages);
-                mbar_wait(b_vfull(sv), int((gi / kVStages) & 1));
-                const uint32_t va = s0 + kV0 + sv * kKVTile;
-                for (int st = 0; st < 2; ++st) {
-                    mbar_wait(b_pfull(st, b), int((gi >> 1) & 1));
-                    if (st == 0) TR(4, gi);
-                    fence_after();
-                    const uint32_t pa = s0 + kP0 + (st * 2 + b) * kPTile;
-#pragma unroll
-                    for (int k = 0; k < BN / 16; ++k)  // K = keys: A = P (K-major), B = V (MN-major)
-                        mma(tmem + 256 + st * D, desc_k(pa + k * 32), desc_mn(va + k * 16 * 128), id_pv,
-                            (!first || k > 0) ? 1u : 0u);
-                    commit(b_pvdone(st, b));
-                }
-                commit(b_vempty(sv));
+            // cursor over the flattened (item, tile) sequence of this CTA
+            struct Cur {
+                int w, j, t, n;
+                long gi;
             };
-            long g = 0;
-            int j = 0;
-            for (int w = blockIdx.x; w < args.n_work; w += gridDim.x, ++j) {
-                const Item it = item(w);
-                mbar_wait(b_qfull, j & 1);
-                TR(9, j);
-                for (int t = 0; t < it.n_tiles; ++t) {
-                    const long gi = g + t;
-                    const int sk = int(gi % kKStages), b = int(gi & 1);
-                    mbar_wait(b_kfull(sk), int((gi / kKStages) & 1));
-                    TR(2, gi);
-                    const uint32_t ka = s0 + kK0 + sk * kKVTile;
-                    for (int st = 0; st < 2; ++st) {
-                        mbar_wait(b_sfree(st, b), int((gi >> 1) & 1) ^ 1);
-                        fence_after();
-                        const uint32_t qa = s0 + kQOff + st * kQTile;
-#pragma unroll
-                        for (int k = 0; k < D / 16; ++k)  // K = head dim: A = Q_s, B = K (both K-major)
-                            mma(tmem + (st * 2 + b) * BN, desc_k(qa + (k >> 2) * kQHalf + (k & 3) * 32),
-                                desc_k(ka + (k >> 2) * kKVHalf + (k & 3) * 32), id_qk, k > 0 ? 1u : 0u);
-                        commit(b_sfull(st, b));
-                    }
-                    commit(b_kempty(sk));
-                    TR(3, gi);
-                    if (t + 1 == it.n_tiles) commit(b_qempty);
-                    if (t == 1) mbar_wait(b_ofree(0), (j & 1) ^ 1), mbar_wait(b_ofree(1), (j & 1) ^ 1);  // item j-1's epilogue read O
-                    if (t > 0) pv(gi - 1, t == 1);
+            auto first_tile = [&](Cur& c) {
+                c.w = blockIdx.x, c.j = 0, c.t = 0, c.gi = 0;
+                c.n = c.w < args.n_work ? item(c.w).n_tiles : 0;
+                return c.w < args.n_work;
+            };
+            auto advance = [&](Cur c) {
+                ++c.gi;
+                if (++c.t == c.n) {
+                    c.t = 0, c.w += gridDim.x, ++c.j;
+                    c.n = c.w < args.n_work ? item(c.w).n_tiles : 0;
                 }
-                if (it.n_tiles == 1) mbar_wait(b_ofree(0), (j & 1) ^ 1), mbar_wait(b_ofree(1), (j & 1) ^ 1);
-                pv(g + it.n_tiles - 1, it.n_tiles == 1);
-                g += it.n_tiles;
+                return c;
+            };
+            auto qk = [&](const Cur& c, int st) {  // S_st = Q_st . K(c)^T
+                const int sk = int(c.gi % kKStages);
+                if (st == 0) {
+                    mbar_wait(b_kfull(sk), int((c.gi / kKStages) & 1));
+                    TR(2, c.gi);
+                }
+                if (c.t == 0) mbar_wait(b_qfull(st), c.j & 1);
+                fence_after();
+                const uint32_t qa = s0 + kQOff + st * kQTile, ka = s0 + kK0 + sk * kKVTile;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k)  // K = head dim: A = Q_st, B = K (both K-major)
+                    mma(tmem + st * BN, desc_k(qa + (k >> 2) * kQHalf + (k & 3) * 32), desc_k(ka + (k >> 2) * kKVHalf + (k & 3) * 32),
+                        id_qk, k > 0 ? 1u : 0u);
+                commit(b_sfull(st));
+                if (c.t + 1 == c.n) commit(b_qempty(st));
+                if (st == 1) commit(b_kempty(sk));
+            };
+            auto pv = [&](const Cur& c, int st) {  // O_st += P_st . V(c), P_st from TMEM
+                const int sv = int(c.gi % kVStages);
+                if (st == 0) mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
+                mbar_wait(b_pfull(st), int(c.gi & 1));
+                if (st == 0) TR(4, c.gi);
+                if (c.t == 0) mbar_wait(b_ofree(st), (c.j & 1) ^ 1);  // the previous item's epilogue read O_st
+                fence_after();
+                const uint32_t va = s0 + kV0 + sv * kKVTile;
+#pragma unroll
+                for (int k = 0; k < BN / 16; ++k)  // K = keys: A = P (TMEM, 8 columns per 16 keys), B = V (MN-major)
+                    mma_ts(tmem + 256 + st * D, tmem + st * BN + k * 8, desc_mn(va + k * 16 * 128), id_pv,
+                           (c.t > 0 || k > 0) ? 1u : 0u);
+                commit(b_pvdone(st));
+                if (st == 1) commit(b_vempty(sv));
+            };
+            Cur cur;
+            if (first_tile(cur)) {
+                qk(cur, 0);
+                qk(cur, 1);
+                while (true) {
+                    const Cur nxt = advance(cur);
+                    const bool more = nxt.w < args.n_work;
+                    // PV_s(t) then QK_s(t+1): the tensor pipe executes in issue order, so QK_s(t+1)
+                    // overwrites S_s / P_s only after PV_s(t) has consumed P_s
+                    pv(cur, 0);
+                    if (more) qk(nxt, 0);
+                    pv(cur, 1);
+                    if (more) qk(nxt, 1);
+                    TR(3, cur.gi);
+                    if (!more) break;
+                    cur = nxt;
+                }
             }
         }
+    }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
         // ---- softmax: stream st = Q tile, lane quarter q4 = warp % 4 (TMEM lanes = rows); every
-        // thread owns one query row and all 64 columns of each S tile
-        const int st = (warp - 2) >> 2, q4 = warp & 3;
+        // thread owns one query row and all 128 columns of each S tile
+        const int st = (warp - 4) >> 2, q4 = warp & 3;
         const int r = q4 * 32 + lane;
         const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+        const uint32_t tS = tmem + st * BN + lane_off;
         const uint32_t tO = tmem + 256 + st * D + lane_off;
         const float sl2 = a.scale * 1.4426950408889634f;
         long g = 0;
@@ -358,38 +391,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m_run = -INFINITY, l_run = 0.f;
             for (int t = 0; t < it.n_tiles; ++t) {
                 const long gi = g + t;
-                const int b = int(gi & 1);
                 const bool ctx = t < it.n_ctx_tiles;
                 const int base_j = ctx ? t * BN : sq.n_ctx + (t - it.n_ctx_tiles) * BN;  // key index of column 0
                 const int seg_end = ctx ? sq.n_ctx : sq.n_ctx + sq.n_own;
-                mbar_wait(b_sfull(st, b), int((gi >> 1) & 1));
-                if (warp == 2 && lane == 0) TR(5, gi);
+                mbar_wait(b_sfull(st), int(gi & 1));
+                if (warp == 4 && lane == 0) TR(5, gi);
                 fence_after();
-                uint32_t u[64];
-                tmem_ld32_async(tmem + (st * 2 + b) * BN + lane_off, u);
-                tmem_ld32_async(tmem + (st * 2 + b) * BN + lane_off + 32, u + 32);
+                uint32_t u[BN];
+#pragma unroll
+                for (int c = 0; c < BN; c += 32) tmem_ld32_async(tS + c, u + c);
                 tmem_wait_ld();
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(b_sfree(st, b));
-                float* s = reinterpret_cast<float*>(u);
                 float mx = -INFINITY;
                 if (ctx && base_j + BN <= sq.n_ctx) {  // full prefix tile: nothing masked
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) mx = fmaxf(mx, s[c]);
+                    for (int c = 0; c < BN; ++c) mx = fmaxf(mx, __uint_as_float(u[c]));
                 } else {
                     const int lim = min(seg_end, causal + 1) - base_j;  // columns [0, lim) visible
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        s[c] = c < lim ? s[c] : -INFINITY;
-                        mx = fmaxf(mx, s[c]);
+                    for (int c = 0; c < BN; ++c) {
+                        if (c >= lim) u[c] = 0xff800000u;  // -inf
+                        mx = fmaxf(mx, __uint_as_float(u[c]));
                     }
                 }
                 mx *= sl2;  // scale > 0: the max commutes with it
                 // conditional rescale: keep the running max unless it grows by more than 8 (x256)
                 const bool grow = mx > m_run + 8.f;
                 if (t > 0 && __any_sync(0xffffffffu, grow)) {
-                    mbar_wait(b_pvdone(st, int((gi - 1) & 1)), int(((gi - 1) >> 1) & 1));  // O is stable after P(t-1).V
+                    mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
                     fence_after();
                     const float corr = grow ? ex2(m_run - mx) : 1.f;
 #pragma unroll
@@ -400,38 +428,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int i = 0; i < 32; ++i) o[i] *= corr;
                         tmem_st32(tO + c, o);
                     }
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     if (grow) l_run *= corr;
                 }
                 if (grow) m_run = mx;
                 const float nb = m_run == -INFINITY ? 0.f : -m_run;
-                // P(gi) -> smem buffer [st][b] (free once P(gi-2).V has completed)
-                if (gi >= 2) mbar_wait(b_pvdone(st, b), int(((gi - 2) >> 1) & 1));
-                const uint32_t pbuf = s0 + kP0 + (st * 2 + b) * kPTile;
+                // P -> bf16 pairs over S's first 64 columns (this thread's row only)
                 float sum = 0.f;
 #pragma unroll
-                for (int c = 0; c < 64; c += 8) {
-                    float p[8];
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        p[i] = live ? ex2(fmaf(s[c + i], sl2, nb)) : 0.f;
-                        sum += p[i];
+                    for (int i = 0; i < 32; i += 2) {
+                        const float p0 = live ? ex2(fmaf(__uint_as_float(u[c + i]), sl2, nb)) : 0.f;
+                        const float p1 = live ? ex2(fmaf(__uint_as_float(u[c + i + 1]), sl2, nb)) : 0.f;
+                        sum += p0 + p1;
+                        pk[i >> 1] = pack_bf16x2(p0, p1);
                     }
-                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(pbuf + sw_off(r, c >> 3, kPTile)),
-                                 "r"(pack_bf16x2(p[0], p[1])), "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])),
-                                 "r"(pack_bf16x2(p[6], p[7]))
-                                 : "memory");
+                    tmem_st16(tS + (c >> 1), pk);
                 }
                 l_run += sum;
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(b_pfull(st, b));
-                if (warp == 2 && lane == 0) TR(6, gi);
+                if (lane == 0) mbar_arrive(b_pfull(st));
+                if (warp == 4 && lane == 0) TR(6, gi);
             }
             // ---- epilogue: O / l -> bf16 row, then O free for the next item
             const long gl = g + it.n_tiles - 1;
-            mbar_wait(b_pvdone(st, int(gl & 1)), int((gl >> 1) & 1));
+            mbar_wait(b_pvdone(st), int(gl & 1));
             fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16* dst = a.out + long(sq.q_row0 + tok) * qw + (it.kvh * G + r % G) * D;
@@ -450,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(b_ofree(st));
-            if (warp == 2 && lane == 0) TR(7, j);
+            if (warp == 4 && lane == 0) TR(7, j);
             g += it.n_tiles;
         }
     }
