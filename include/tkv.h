@@ -125,9 +125,12 @@ int tkv_store_load_kv_file(tkv_store* s, const char* path, int* table_id);
 int tkv_store_precompute(tkv_store* s, const tkv_engine* e, const char* out_dir);
 /* copy a table into pool pages (one miss), read the landed bytes back (bytes-exact check) */
 int tkv_store_fetch(tkv_store* s, int table_id, int copy_engine, void* host_out, size_t bytes);
-/* assemble() on the GPU (attention.hpp:300-362): k_out/v_out [L][total][kv_dim] in the model's
- * serving dtype (f32 for f32 models, bf16 otherwise); *total_tokens gets the prefix length */
-int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, void* k_out, void* v_out, int* total_tokens);
+/* assemble() on the GPU (attention.hpp:300-362): k_out/v_out [L][total][kv_dim] (dense, row stride
+ * total) in the model's serving dtype (f32 for f32 models, bf16 otherwise), each buffer holding
+ * cap_tokens rows per layer at least; *total_tokens gets the prefix length (also on the
+ * too-small error, so a caller can size and retry; null outputs = length only) */
+int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, size_t cap_tokens, void* k_out, void* v_out,
+                       int* total_tokens);
 /* arena footprint */
 int tkv_store_info(const tkv_store* s, size_t* tables, size_t* arena_bytes, size_t* free_pages);
 

@@ -693,9 +693,16 @@ int tkv_store_fetch(tkv_store* s, int table_id, int copy_engine, void* host_out,
     });
 }
 
-int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, void* k_out, void* v_out, int* total_tokens) {
+int tkv_store_assemble(tkv_store* s, const int32_t* tables, int n_tables, size_t cap_tokens, void* k_out, void* v_out,
+                       int* total_tokens) {
     return guard([&] {
         need(s && (tables || n_tables == 0), "null argument");
+        long need_tokens = 0;
+        for (int i = 0; i < n_tables; ++i)
+            if (const tkv::TableImage* img = s->arena->find(tables[i])) need_tokens += img->tokens;
+        if (total_tokens) *total_tokens = int(need_tokens);
+        need(!(k_out || v_out) || size_t(need_tokens) <= cap_tokens, "output buffers hold fewer tokens than the prefix");
+        if (!k_out && !v_out) return;
         set_device(s->model->device);
         tkv::Model& model = *s->model->m;
         const auto& c = model.cfg();

@@ -8,6 +8,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace tkv {
 
 namespace {
@@ -108,7 +111,89 @@ __global__ void gather_rope_kernel(const uint8_t* __restrict__ pool, long page_b
     }
 }
 
+// Serving fast path (bf16 image -> bf16 slab, one layer): CTA = one chunk of <= kChunkRows rows
+// of ONE table segment (host-built list: no per-row segment search), warp = one row; every lane
+// issues all of its 16-byte K and V loads (page addressing by shift: power-of-two pages) before
+// rotating K and storing.
+constexpr int kChunkRows = 8;
+
+__global__ void __launch_bounds__(256) gather_rope_bf16_kernel(const uint8_t* __restrict__ pool, int page_shift,
+                                                               const int32_t* __restrict__ page_ids,
+                                                               const GatherSeg* __restrict__ segs, const int4* __restrict__ chunks,
+                                                               int L, int l, int kvdim, int head_dim,
+                                                               const float* __restrict__ cos_f, const float* __restrict__ sin_f,
+                                                               uint8_t* __restrict__ out_k, uint8_t* __restrict__ out_v) {
+    const int4 ch = chunks[blockIdx.x];  // {seg, t0, rows, 0}
+    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (r >= ch.z) return;
+    const GatherSeg sg = segs[ch.x];
+    const int t = ch.y + r;
+    const long pos = sg.pos0 + t;
+    const int vpr = kvdim >> 3;  // 16-byte vectors per row (8 bf16)
+    const long row_in = long(kvdim) * 2;
+    const long pmask = (1L << page_shift) - 1;
+    const int half = head_dim >> 1;
+    const int32_t* pages = page_ids + sg.page_off;
+    for (int v0 = 0; v0 < vpr; v0 += 128) {
+        uint4 kv[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const long base = ((long(c) * L + l) * sg.tokens + t) * row_in;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int vi = v0 + lane + 32 * q;
+                if (vi < vpr) {
+                    const long off = base + long(vi) * 16;
+                    kv[c][q] = *reinterpret_cast<const uint4*>(pool + (long(pages[off >> page_shift]) << page_shift) + (off & pmask));
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int vi = v0 + lane + 32 * q;
+            if (vi >= vpr) continue;
+            uint4 w = kv[0][q];
+            if (pos != 0) {
+                const int k0 = ((vi * 8) % head_dim) >> 1;  // first rotary pair of this vector
+                const float4 c = *reinterpret_cast<const float4*>(cos_f + pos * half + k0);
+                const float4 sn = *reinterpret_cast<const float4*>(sin_f + pos * half + k0);
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+                const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 ab = unpack_bf16x2(wp[e]);
+                    wp[e] = pack_bf16x2(fmaf(ab.x, cc[e], -ab.y * ss[e]), fmaf(ab.x, ss[e], ab.y * cc[e]));
+                }
+            }
+            const long o = (long(sg.out_row0 + t) * kvdim + long(vi) * 8) * 2;
+            *reinterpret_cast<uint4*>(out_k + o) = w;
+            *reinterpret_cast<uint4*>(out_v + o) = kv[1][q];
+        }
+    }
+}
+
 }  // namespace
+
+int gather_chunks(const GatherSeg* segs, int n_segs, std::vector<int4>& out) {
+    out.clear();
+    for (int s = 0; s < n_segs; ++s)
+        for (int t = 0; t < segs[s].tokens; t += kChunkRows) out.push_back(make_int4(s, t, std::min(kChunkRows, segs[s].tokens - t), 0));
+    return int(out.size());
+}
+
+void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
+                             const int4* d_chunks, int n_chunks, int L, int l, int kvdim, int head_dim, const float* cos_f,
+                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s) {
+    if (n_chunks <= 0) return;
+    if (kvdim % 8 || head_dim % 8) throw std::invalid_argument("gather: kv row must hold whole 16-byte vectors");
+    if (page_bytes & (page_bytes - 1)) throw std::invalid_argument("gather fast path: page size must be a power of two");
+    int shift = 0;
+    while ((size_t(1) << shift) < page_bytes) ++shift;
+    gather_rope_bf16_kernel<<<n_chunks, 32 * kChunkRows, 0, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim,
+                                                                 head_dim, cos_f, sin_f, static_cast<uint8_t*>(out_k),
+                                                                 static_cast<uint8_t*>(out_v));
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
                         int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,

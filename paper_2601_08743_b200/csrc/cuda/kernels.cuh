@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace tkv {
 
 enum class DType : int { f32 = 0, bf16 = 1, f64 = 2 };
@@ -48,6 +50,12 @@ void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d
                         int n_segs, int total_rows, int L, int kvdim, int head_dim, DType in_dt, DType out_dt,
                         const double* cos_d, const double* sin_d, const float* cos_f, const float* sin_f,
                         void* out_k, void* out_v, long out_rows, cudaStream_t s, int l0 = 0, int nl = -1);
+// Serving fast path: bf16 image -> bf16 one-layer slab for layer l, one CTA per chunk of <= 8 rows
+// of one segment (gather_chunks builds the list once per window on the host).
+int gather_chunks(const GatherSeg* segs, int n_segs, std::vector<int4>& out);
+void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
+                             const int4* d_chunks, int n_chunks, int L, int l, int kvdim, int head_dim, const float* cos_f,
+                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s);
 // (l0, nl): gather only layers [l0, l0 + nl) of the L-layer images into out layers [0, nl) — the
 // serving path streams one layer of prefix at a time just before that layer's attention.
 

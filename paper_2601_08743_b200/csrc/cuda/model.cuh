@@ -83,6 +83,8 @@ struct FwdArgs {
     const int32_t* gather_pages = nullptr;  // device
     const GatherSeg* gather_segs = nullptr; // device
     int gather_n_segs = 0, gather_rows = 0;
+    const int4* gather_chunks = nullptr;    // device: {seg, t0, rows, 0} (bf16 fast path)
+    int gather_n_chunks = 0;
     DType gather_in = DType::bf16;
     void* kraw_out = nullptr;           // optional [L][M][kv_dim] pre-rotation keys (offline encode)
     void* v_out = nullptr;              // optional [L][M][kv_dim]

@@ -430,10 +430,16 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         StagingRing& ring = model_.ring();
         const GatherSeg* d_segs_s = nullptr;
         const int32_t* d_pages_s = nullptr;
+        const int4* d_chunks_s = nullptr;
+        int n_chunks_s = 0;
         DType in_dt_s = DType::bf16;
         if (ctx_rows > 0 && stream_ctx && M > 0) {
             d_segs_s = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
             d_pages_s = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
+            std::vector<int4> chunks;
+            n_chunks_s = gather_chunks(segs.data(), int(segs.size()), chunks);
+            d_chunks_s = static_cast<const int4*>(ring.upload(chunks.data(), chunks.size() * sizeof(int4), cs_));
+            R.meta_bytes += chunks.size() * sizeof(int4);
             R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
             for (const auto& qs : qsegs)
                 if (!qs.empty()) {
@@ -488,6 +494,8 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 fa.gather_n_segs = int(segs.size());
                 fa.gather_rows = ctx_rows;
                 fa.gather_in = in_dt_s;
+                fa.gather_chunks = d_chunks_s;
+                fa.gather_n_chunks = n_chunks_s;
             }
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
             fa.logit_rows_host = logit_rows.data();

@@ -91,7 +91,7 @@ _sig("tkv_store_put", _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp)
 _sig("tkv_store_load_kv_file", _vp, C.c_char_p, C.POINTER(C.c_int))
 _sig("tkv_store_precompute", _vp, _vp, C.c_char_p)
 _sig("tkv_store_fetch", _vp, C.c_int, C.c_int, _vp, C.c_size_t)
-_sig("tkv_store_assemble", _vp, _i32p, C.c_int, _vp, _vp, C.POINTER(C.c_int))
+_sig("tkv_store_assemble", _vp, _i32p, C.c_int, C.c_size_t, _vp, _vp, C.POINTER(C.c_int))
 _sig("tkv_store_info", _vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
 _sig("tkv_store_bind_engine", _vp, _vp)
 _sig("tkv_serve_options_default", C.POINTER(tkv_serve_options), res=None)
@@ -393,14 +393,18 @@ class Store:
         _check(_lib.tkv_store_fetch(self._h, table_id, copy_engine, out.ctypes.data, nbytes))
         return out
 
-    def assemble(self, tables, total_hint):
+    def assemble(self, tables, total_hint=None):
+        """[L][total][kv_dim] rotated K and V of the tables concatenated in order (total_hint unused:
+        the prefix length is asked first)."""
         L, kvd = self.model.cfg.num_layers, self.model.kv_dim
         edt = np.uint16 if self.model.dtype == 1 else np.float32
-        k = np.zeros((L, max(1, total_hint), kvd), edt)
-        v = np.zeros_like(k)
         t = _arr(tables, np.int32)
         total = C.c_int()
-        _check(_lib.tkv_store_assemble(self._h, _ptr(t, C.c_int32), len(t), k.ctypes.data, v.ctypes.data,
+        _check(_lib.tkv_store_assemble(self._h, _ptr(t, C.c_int32), len(t), 0, None, None, C.byref(total)))
+        n = max(1, total.value)
+        k = np.zeros((L, n, kvd), edt)
+        v = np.zeros_like(k)
+        _check(_lib.tkv_store_assemble(self._h, _ptr(t, C.c_int32), len(t), n, k.ctypes.data, v.ctypes.data,
                                        C.byref(total)))
         return k[:, :total.value], v[:, :total.value]
 

@@ -305,3 +305,25 @@ def test_bf16_executor_argmax_matches_bf16_oracle():
             assert res["argmax"][i] == int(np.argmax(lg))
     s.close()
     m.close()
+
+
+def test_bf16_serving_path_matches_per_query_forward():
+    """The Llama-shaped serving path (bf16 arena from the GPU precompute, layer-streamed prefix
+    gather with the chunked bf16 kernel, batched tcgen05 attention over many sequences) against
+    each query run alone: assemble() of its tables + one-sequence forward, same weights."""
+    kw = dict(num_layers=2, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=330, ffn_dim=512, mlp="swiglu",
+              norm="rms")
+    m = N.Model(dtype="bf16", **kw)
+    s = N.Store(m, page_bytes=64 << 10, n_pages=2048)
+    eng = N.Engine(demo_path("demo_schema.json"))
+    s.precompute(eng)
+    qs = _demo_queries(24)
+    res = s.serve(qs, capacity=6, b_c=8, b_m=2, want_logits=True)
+    for i, qi in enumerate(res["order"]):
+        tables, suffix = qs[qi]
+        k, v = s.assemble(tables, 1024)
+        ref = m.forward(suffix, mode=0, ctx_k=k, ctx_v=v)
+        err = np.abs(res["logits"][i] - ref["logits"]).max()
+        assert err <= 3e-2, (i, err)
+    s.close()
+    m.close()
