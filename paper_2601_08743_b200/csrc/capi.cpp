@@ -362,6 +362,26 @@ int tkv_rerank(const uint64_t* inc, size_t n, size_t words, uint64_t seed, int f
     });
 }
 
+int tkv_rerank_device(int device, const uint64_t* inc, size_t n, size_t words, uint64_t seed, int fixed_first,
+                      uint64_t* perm) {
+    return guard([&] {
+        need(inc && perm, "null argument");
+        set_device(device);
+        cudaStream_t st;
+        TKV_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        std::vector<size_t> p;
+        try {
+            p = tkv::rerank_device(inc, n, words, seed,
+                                   fixed_first ? tablekv::AnchorMode::fixed_first : tablekv::AnchorMode::seeded, st);
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaStreamDestroy(st);
+        std::copy(p.begin(), p.end(), perm);
+    });
+}
+
 // ------------------------------------------------------------------ cache
 int tkv_cache_create(size_t capacity, int policy, const int32_t* counts, size_t n, tkv_cache** out) {
     return guard([&] {

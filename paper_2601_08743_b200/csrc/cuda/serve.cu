@@ -68,7 +68,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace
 
 BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::vector<int>& suffix_len,
-                      const ServeOptions& opts, const Arena& arena) {
+                      const ServeOptions& opts, const Arena& arena, cudaStream_t stream) {
     BatchTrace bt;
     int n_bits = 0;
     for (const auto& q : tables)
@@ -80,7 +80,15 @@ BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::ve
         r.tables = tables[i];
         recs.push_back(std::move(r));
     }
-    bt.order = tablekv::serving_order(recs, opts.run);
+    if (opts.run.rerank_on && recs.size() >= kDeviceRerankMin) {
+        const size_t words = recs.front().inc.words.size();
+        std::vector<uint64_t> packed(recs.size() * words, 0);
+        for (size_t i = 0; i < recs.size(); ++i)
+            if (!recs[i].tables.empty()) std::copy(recs[i].inc.words.begin(), recs[i].inc.words.end(), packed.begin() + long(i * words));
+        bt.order = rerank_device(packed.data(), recs.size(), words, opts.run.seed, opts.run.anchor, stream);
+    } else {
+        bt.order = tablekv::serving_order(recs, opts.run);
+    }
     std::vector<tablekv::SimQuery> sims;
     for (size_t i : bt.order) sims.push_back({recs[i].query_id, tables[i], suffix_len[i]});
     bt.plan = tablekv::schedule(std::move(sims), opts.run.b_c, opts.run.b_m);
@@ -174,7 +182,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     std::vector<std::vector<int>> qt;
     std::vector<int> qn;
     for (const auto& q : queries) qt.push_back(q.tables), qn.push_back(int(q.suffix.size()));
-    BatchTrace bt = plan_batch(qt, qn, opts, arena_);
+    BatchTrace bt = plan_batch(qt, qn, opts, arena_, cs_);
     R.order = std::move(bt.order);
     const tablekv::BatchPlan& plan = bt.plan;
     const tablekv::Trace& tr = bt.trace;

@@ -82,7 +82,11 @@ struct BatchTrace {
     bool managed = true;
 };
 BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::vector<int>& suffix_len,
-                      const ServeOptions& opts, const Arena& arena);
+                      const ServeOptions& opts, const Arena& arena, cudaStream_t s = nullptr);
+// rerank_packed (csrc/host/rerank.cpp) on the GPU: identical permutation, one CTA runs the chain
+std::vector<size_t> rerank_device(const uint64_t* inc, size_t n, size_t words, uint64_t seed, tablekv::AnchorMode mode,
+                                  cudaStream_t s);
+constexpr size_t kDeviceRerankMin = 512;  // batches at least this large rerank on the GPU
 // table -> [first, last] windows during which the executor keeps it published for peers
 std::unordered_map<int, std::vector<std::pair<int, int>>> residency_intervals(const BatchTrace& bt);
 

@@ -4,6 +4,7 @@
 // the single-threaded scan for any thread count.
 #include <algorithm>
 #include <atomic>
+#include <barrier>
 #include <bit>
 #include <thread>
 
@@ -88,34 +89,59 @@ std::vector<size_t> rerank_packed(const std::uint64_t* inc, size_t n, size_t wor
         if (threads <= 0) threads = int(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
         if (m < 4096) threads = 1;
         std::vector<Best> part(static_cast<size_t>(threads));
-        while (!remaining.empty()) {
-            const std::uint64_t* a = inc + cur * words;
-            auto scan = [&](size_t lo, size_t hi, Best& b) {
-                for (size_t k = lo; k < hi; ++k) {
-                    const std::uint64_t* c = inc + live[remaining[k]] * words;
-                    std::uint64_t d = 0;
-                    for (size_t w = 0; w < words; ++w) d += std::uint64_t(std::popcount(a[w] ^ c[w]));
-                    if (d < b.d) b = {d, k};  // k ascending => first minimum = lowest slot
+        const std::uint64_t* a = nullptr;
+        auto scan = [&](size_t lo, size_t hi, Best& b) {
+            for (size_t k = lo; k < hi; ++k) {
+                const std::uint64_t* c = inc + live[remaining[k]] * words;
+                std::uint64_t d = 0;
+                for (size_t w = 0; w < words; ++w) d += std::uint64_t(std::popcount(a[w] ^ c[w]));
+                if (d < b.d) b = {d, k};  // k ascending => first minimum = lowest slot
+            }
+        };
+        auto chunk_of = [&](int t, size_t& lo, size_t& hi) {
+            const size_t chunk = (remaining.size() + size_t(threads) - 1) / size_t(threads);
+            lo = std::min(remaining.size(), size_t(t) * chunk);
+            hi = std::min(remaining.size(), lo + chunk);
+        };
+        // persistent workers, two barrier phases per chain step (scan, then the reduction on this thread)
+        std::barrier sync(threads);
+        bool done = false;
+        std::vector<std::thread> pool;
+        for (int t = 1; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                for (;;) {
+                    sync.arrive_and_wait();
+                    if (done) return;
+                    size_t lo, hi;
+                    chunk_of(t, lo, hi);
+                    part[size_t(t)] = Best{};
+                    scan(lo, hi, part[size_t(t)]);
+                    sync.arrive_and_wait();
                 }
-            };
+            });
+        while (!remaining.empty()) {
+            a = inc + cur * words;
             Best best;
             if (threads == 1) {
                 scan(0, remaining.size(), best);
             } else {
-                std::vector<std::thread> pool;
-                const size_t chunk = (remaining.size() + size_t(threads) - 1) / size_t(threads);
-                for (int t = 0; t < threads; ++t) {
-                    part[size_t(t)] = Best{};
-                    const size_t lo = size_t(t) * chunk, hi = std::min(remaining.size(), lo + chunk);
-                    if (lo < hi) pool.emplace_back(scan, lo, hi, std::ref(part[size_t(t)]));
-                }
-                for (auto& th : pool) th.join();
+                sync.arrive_and_wait();
+                size_t lo, hi;
+                chunk_of(0, lo, hi);
+                part[0] = Best{};
+                scan(lo, hi, part[0]);
+                sync.arrive_and_wait();
                 for (const Best& b : part)
                     if (best.better(b)) best = b;
             }
             cur = live[remaining[best.slot]];
             out.push_back(cur);
             remaining.erase(remaining.begin() + long(best.slot));
+        }
+        if (threads > 1) {
+            done = true;
+            sync.arrive_and_wait();
+            for (auto& th : pool) th.join();
         }
     }
     out.insert(out.end(), empty.begin(), empty.end());

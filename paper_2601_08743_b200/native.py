@@ -73,6 +73,7 @@ _sig("tkv_trie_query", _vp, _i32p, C.c_size_t, C.c_size_t, C.POINTER(C.c_int), C
      C.POINTER(C.c_int), _u64p)
 _sig("tkv_trie_match_all", _vp, _i32p, C.c_size_t, _i64p, C.c_size_t, C.POINTER(C.c_size_t), _u64p)
 _sig("tkv_rerank", _u64p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int, C.c_int, _u64p)
+_sig("tkv_rerank_device", C.c_int, _u64p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int, _u64p)
 _sig("tkv_cache_create", C.c_size_t, C.c_int, _i32p, C.c_size_t, C.POINTER(_vp))
 _sig("tkv_cache_destroy", _vp, res=None)
 _sig("tkv_cache_get", _vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int))
@@ -226,6 +227,15 @@ def rerank(table_sets, n_bits, seed=1, mode="seeded", threads=0):
     perm = np.zeros(len(table_sets), np.uint64)
     _check(_lib.tkv_rerank(_ptr(inc, C.c_uint64), inc.shape[0], inc.shape[1], seed, int(mode == "fixed_first"), threads,
                            _ptr(perm, C.c_uint64)))
+    return [int(x) for x in perm]
+
+
+def rerank_device(table_sets, n_bits, seed=1, mode="seeded", device=0):
+    """rerank on the GPU: the same permutation as rerank() (rerank.cpp:55-94)."""
+    inc = pack_incidence(table_sets, n_bits)
+    perm = np.zeros(len(table_sets), np.uint64)
+    _check(_lib.tkv_rerank_device(device, _ptr(inc, C.c_uint64), inc.shape[0], inc.shape[1], seed,
+                                  int(mode == "fixed_first"), _ptr(perm, C.c_uint64)))
     return [int(x) for x in perm]
 
 

@@ -327,3 +327,17 @@ def test_bf16_serving_path_matches_per_query_forward():
         assert err <= 3e-2, (i, err)
     s.close()
     m.close()
+
+
+@pytest.mark.parametrize("n,n_bits,seed", [(1, 12, 1), (64, 12, 1), (600, 200, 3), (3000, 200, 7), (9000, 660, 1),
+                                           (2500, 4096, 5)])
+def test_device_rerank_identical_to_reference_chain(n, n_bits, seed):
+    """rerank on the GPU (one CTA, (distance, slot) argmin) == the host chain pinned to the
+    reference's goldens (strict-< ties to the lowest slot, empty sets last, seeded anchor)."""
+    rng = np.random.default_rng(seed)
+    sets = []
+    for i in range(n):
+        k = int(rng.integers(0, 6))  # small sets: many distance ties
+        sets.append(sorted(set(rng.integers(0, min(n_bits, 40), k).tolist())) if i % 17 else [])
+    for mode in ("seeded", "fixed_first"):
+        assert N.rerank_device(sets, n_bits, seed=seed, mode=mode) == N.rerank(sets, n_bits, seed=seed, mode=mode)
