@@ -74,6 +74,21 @@ def _worker(rank, world, port, out_dir):
     out["serve"] = {k: [base[k], peer[k]] for k in ("order", "trace", "counters", "argmax")}
     out["bytes"] = {k: peer[k] for k in ("h2d_bytes", "peer_routed_bytes", "peer_bytes", "peer_fallback_bytes")}
     out["base_h2d"] = base["h2d_bytes"]
+    # routing: rank 0 serves cluster A (tables 0-3) then cluster B (4-7), rank 1 the reverse, so
+    # each rank's switch-over misses find the other cluster resident on the peer (the host-side
+    # residency directory routes them to the peer path)
+    qa = [([0, 1, 2, 3], r) for _, r in qs[:8]]
+    qb = [([4, 5, 6, 7], r) for _, r in qs[8:16]]
+    lead, peer_batch = (qa + qb, qb + qa) if rank == 0 else (qb + qa, qa + qb)
+    kw2 = dict(rerank_on=0, capacity=4, b_c=2, b_m=1)
+    s.peer_plan(0, peer_batch)
+    dist.barrier()
+    base2 = s.serve(lead, **kw2)
+    dist.barrier()
+    shifted = s.serve(lead, peer_fetch=1, **kw2)
+    out["shifted"] = {k: shifted[k] for k in ("h2d_bytes", "peer_routed_bytes", "peer_bytes", "peer_fallback_bytes")}
+    out["shifted_same"] = all(base2[k] == shifted[k] for k in ("order", "trace", "counters", "argmax"))
+    out["shifted_base_h2d"] = base2["h2d_bytes"]
     out["free_pages"] = s.info()["free_pages"]
     json.dump(out, open(os.path.join(out_dir, "rank%d.json" % rank), "w"))
     dist.barrier()
@@ -107,3 +122,9 @@ def test_peer_fetch_leaves_trace_and_first_tokens_unchanged(two_ranks):
         assert b["h2d_bytes"] + b["peer_routed_bytes"] == r["base_h2d"]
         assert b["peer_bytes"] + b["peer_fallback_bytes"] == b["peer_routed_bytes"]
         assert r["free_pages"] == 4096
+        assert r["shifted_same"]
+        b = r["shifted"]
+        assert b["h2d_bytes"] + b["peer_routed_bytes"] == r["shifted_base_h2d"]
+        assert b["peer_bytes"] + b["peer_fallback_bytes"] == b["peer_routed_bytes"]
+    for r in two_ranks:
+        assert r["shifted"]["peer_routed_bytes"] > 0, r["shifted"]
