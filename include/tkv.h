@@ -123,6 +123,10 @@ void tkv_store_destroy(tkv_store* s);
 int tkv_store_put(tkv_store* s, int table_id, int tokens, int local_offset, int dtype, const void* payload);
 /* a reference .kv file (FileSlowTier::load, tiered_cache.cpp:49-59) straight into the arena */
 int tkv_store_load_kv_file(tkv_store* s, const char* path, int* table_id);
+/* a precompute directory (<id>.kv f32 reference files and/or <id>.kvb bf16 images) straight into
+ * the pinned arena with `threads` readers (0: 8); e (nullable) checks manifest.json first
+ * (check_manifest, engine.cpp:114-131). Tables already in the arena are skipped. */
+int tkv_store_load_dir(tkv_store* s, const char* dir, const tkv_engine* e, int threads, int* n_loaded);
 /* offline encode of every group on the GPU (precompute_corpus, engine.cpp:83-112) into the arena;
  * out_dir (nullable) also gets <id>.kv files (f32 models: the reference format) + manifest.json */
 int tkv_store_precompute(tkv_store* s, const tkv_engine* e, const char* out_dir);

@@ -623,6 +623,63 @@ int tkv_store_load_kv_file(tkv_store* s, const char* path, int* table_id) {
     });
 }
 
+int tkv_store_load_dir(tkv_store* s, const char* dir, const tkv_engine* e, int threads, int* n_loaded) {
+    return guard([&] {
+        need(s && dir, "null argument");
+        namespace fs = std::filesystem;
+        if (e) tablekv::check_manifest(e->e, dir);  // engine.cpp:114-131: model/tokenizer must match
+        const auto& c = s->model->m->cfg();
+        struct Job {
+            fs::path path;
+            const tkv::TableImage* img;
+        };
+        std::vector<Job> jobs;
+        std::error_code ec;
+        for (const auto& ent : fs::directory_iterator(dir, ec)) {
+            const auto ext = ent.path().extension().string();
+            if (ext != ".kv" && ext != ".kvb") continue;
+            const tkv::DType dt = ext == ".kv" ? tkv::DType::f32 : tkv::DType::bf16;
+            std::ifstream in(ent.path(), std::ios::binary);
+            unsigned char h[24];
+            if (!in.read(reinterpret_cast<char*>(h), 24))
+                throw tablekv::Error(tablekv::Errc::io_error, "truncated KV file: " + ent.path().string());
+            int f[6];
+            for (int i = 0; i < 6; ++i) f[i] = int(tablekv::kvfile::rd32(h + 4 * i));
+            const size_t payload = size_t(2) * f[2] * f[1] * f[3] * f[4] * tkv::dtype_size(dt);
+            if (fs::file_size(ent.path()) != 24 + payload)
+                throw tablekv::Error(tablekv::Errc::io_error, "KV file size mismatch: " + ent.path().string());
+            if (f[2] != c.num_layers || f[3] * f[4] != c.kv_dim())
+                throw tablekv::Error(tablekv::Errc::dimension_mismatch, "KV block shape does not match the model");
+            if (s->arena->find(f[0])) continue;  // already resident in the arena
+            // reserve pinned space now (the arena is single-writer), fill it from the file below
+            jobs.push_back({ent.path(), &s->arena->put(f[0], f[1], f[2], f[3] * f[4], f[5], dt, nullptr)});
+        }
+        if (ec) throw tablekv::Error(tablekv::Errc::io_error, "cannot list " + std::string(dir));
+        // file bytes go straight into pinned memory (no staging copy), files spread over threads
+        const size_t n_thr = std::max<size_t>(1, std::min<size_t>(jobs.size(), threads > 0 ? size_t(threads) : 8));
+        std::vector<std::exception_ptr> errs(n_thr);
+        auto work = [&](size_t w) {
+            try {
+                for (size_t i = w; i < jobs.size(); i += n_thr) {
+                    std::ifstream in(jobs[i].path, std::ios::binary);
+                    in.seekg(24);
+                    if (!in.read(reinterpret_cast<char*>(jobs[i].img->host), std::streamsize(jobs[i].img->bytes)))
+                        throw tablekv::Error(tablekv::Errc::io_error, "short read on " + jobs[i].path.string());
+                }
+            } catch (...) {
+                errs[w] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (size_t w = 1; w < n_thr; ++w) pool.emplace_back(work, w);
+        work(0);
+        for (auto& t : pool) t.join();
+        for (auto& ep : errs)
+            if (ep) std::rethrow_exception(ep);
+        if (n_loaded) *n_loaded = int(jobs.size());
+    });
+}
+
 int tkv_store_bind_engine(tkv_store* s, const tkv_engine* e) {
     return guard([&] {
         need(s && e, "null argument");

@@ -90,6 +90,7 @@ _sig("tkv_store_create", _vp, C.c_size_t, C.c_int, C.POINTER(_vp))
 _sig("tkv_store_destroy", _vp, res=None)
 _sig("tkv_store_put", _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp)
 _sig("tkv_store_load_kv_file", _vp, C.c_char_p, C.POINTER(C.c_int))
+_sig("tkv_store_load_dir", _vp, C.c_char_p, _vp, C.c_int, C.POINTER(C.c_int))
 _sig("tkv_store_precompute", _vp, _vp, C.c_char_p)
 _sig("tkv_store_fetch", _vp, C.c_int, C.c_int, _vp, C.c_size_t)
 _sig("tkv_store_assemble", _vp, _i32p, C.c_int, C.c_size_t, _vp, _vp, C.POINTER(C.c_int))
@@ -391,6 +392,12 @@ class Store:
         tid = C.c_int()
         _check(_lib.tkv_store_load_kv_file(self._h, path.encode(), C.byref(tid)))
         return tid.value
+
+    def load_dir(self, path, engine=None, threads=0):
+        """A precompute directory (.kv f32 / .kvb bf16) into the pinned arena; returns tables loaded."""
+        n = C.c_int()
+        _check(_lib.tkv_store_load_dir(self._h, path.encode(), engine._h if engine else None, threads, C.byref(n)))
+        return n.value
 
     def precompute(self, engine: Engine, out_dir=None):
         _check(_lib.tkv_store_precompute(self._h, engine._h, out_dir.encode() if out_dir else None))

@@ -341,3 +341,31 @@ def test_device_rerank_identical_to_reference_chain(n, n_bits, seed):
         sets.append(sorted(set(rng.integers(0, min(n_bits, 40), k).tolist())) if i % 17 else [])
     for mode in ("seeded", "fixed_first"):
         assert N.rerank_device(sets, n_bits, seed=seed, mode=mode) == N.rerank(sets, n_bits, seed=seed, mode=mode)
+
+
+def test_load_dir_reference_and_bf16_images(tmp_path, f32_store):
+    """Arena loader: the reference .kv directory and our bf16 .kvb precompute
+    directory load straight into pinned memory; landed bytes equal the files' payloads."""
+    m = N.Model(dtype="f32", **C1)
+    s = N.Store(m, page_bytes=4096, n_pages=1024)
+    assert s.load_dir(demo_path("kv"), engine=N.Engine(demo_path("demo_schema.json"))) == 12
+    for t in range(12):
+        raw = open(demo_path("kv", "%d.kv" % t), "rb").read()[24:]
+        assert s.fetch(t, len(raw)).tobytes() == raw
+    s.close()
+    m.close()
+    kw = dict(num_layers=2, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=330, ffn_dim=512, mlp="swiglu",
+              norm="rms")
+    mb = N.Model(dtype="bf16", **kw)
+    eng = N.Engine(demo_path("demo_schema.json"))
+    a = N.Store(mb, page_bytes=64 << 10, n_pages=256)
+    a.precompute(eng, str(tmp_path / "cache"))
+    b = N.Store(mb, page_bytes=64 << 10, n_pages=256)
+    assert b.load_dir(str(tmp_path / "cache"), threads=4) == 12
+    for t in range(12):
+        n = 2 * 2 * len(eng.info["table_tokens"][t]) * 256 * 2
+        assert b.fetch(t, n).tobytes() == a.fetch(t, n).tobytes()
+        assert os.path.getsize(tmp_path / "cache" / ("%d.kvb" % t)) == 24 + n
+    a.close()
+    b.close()
+    mb.close()
