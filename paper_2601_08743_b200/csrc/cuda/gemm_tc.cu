@@ -106,15 +106,36 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v
                           pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
 }
 
+// 32 accumulator columns starting at col0 (a multiple of 32 inside one head of head_dim >= 32):
+// 16 interleaved pairs whose cos/sin are 16 consecutive table entries -> 4 + 4 float4 loads
+// (scalar loads here made the QKV epilogue, not the MMA, the bound of that GEMM)
 __device__ __forceinline__ void rope32(float* v, int col0, int head_dim, int pos, const float* cos_f, const float* sin_f) {
     const int half = head_dim >> 1;
+    if (head_dim & 31) {  // small heads: 32 columns span several heads
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-        const int k = ((col0 + i) % head_dim) >> 1;
-        const float c = cos_f[long(pos) * half + k], s = sin_f[long(pos) * half + k];
-        const float a = v[i], b = v[i + 1];
-        v[i] = fmaf(a, c, -b * s);
-        v[i + 1] = fmaf(a, s, b * c);
+        for (int i = 0; i < 32; i += 2) {
+            const int k = ((col0 + i) % head_dim) >> 1;
+            const float c = cos_f[long(pos) * half + k], s = sin_f[long(pos) * half + k];
+            const float a = v[i], b = v[i + 1];
+            v[i] = fmaf(a, c, -b * s);
+            v[i + 1] = fmaf(a, s, b * c);
+        }
+        return;
+    }
+    const int k0 = (col0 % head_dim) >> 1;
+    const float4* c4 = reinterpret_cast<const float4*>(cos_f + long(pos) * half + k0);
+    const float4* s4 = reinterpret_cast<const float4*>(sin_f + long(pos) * half + k0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 c = __ldg(c4 + q), s = __ldg(s4 + q);
+        const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int i = 8 * q + 2 * e;
+            const float a = v[i], b = v[i + 1];
+            v[i] = fmaf(a, cc[e], -b * ss[e]);
+            v[i + 1] = fmaf(a, ss[e], b * cc[e]);
+        }
     }
 }
 
