@@ -11,6 +11,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <unordered_map>
 
 #include <json.hpp>
 
@@ -367,17 +368,11 @@ int tkv_rerank_device(int device, const uint64_t* inc, size_t n, size_t words, u
     return guard([&] {
         need(inc && perm, "null argument");
         set_device(device);
-        cudaStream_t st;
-        TKV_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        std::vector<size_t> p;
-        try {
-            p = tkv::rerank_device(inc, n, words, seed,
-                                   fixed_first ? tablekv::AnchorMode::fixed_first : tablekv::AnchorMode::seeded, st);
-        } catch (...) {
-            cudaStreamDestroy(st);
-            throw;
-        }
-        cudaStreamDestroy(st);
+        static thread_local std::unordered_map<int, cudaStream_t> streams;  // one per device, kept
+        cudaStream_t& st = streams[device];
+        if (!st) TKV_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const std::vector<size_t> p = tkv::rerank_device(
+            inc, n, words, seed, fixed_first ? tablekv::AnchorMode::fixed_first : tablekv::AnchorMode::seeded, st);
         std::copy(p.begin(), p.end(), perm);
     });
 }

@@ -10,6 +10,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <mutex>
 
 #include "common.cuh"
@@ -409,6 +411,295 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
 }
 
+// ------------------------------------------------------------------ cluster-pair kernel (B multicast)
+// Same warp roles and TMEM double buffer as gemm_tc_persistent, but CTAs run in clusters of two
+// that own vertically adjacent 128 x 256 tiles (same weight columns): each CTA TMA-loads its own
+// A tile and HALF of the shared 256 x 64 B tile with .multicast::cluster into both CTAs' smem, so
+// every weight byte leaves L2 once per pair instead of once per CTA (48 -> 32 KB of L2 reads per
+// CTA per 64-deep K step). Each MMA commit releases the stage in both CTAs (empty count 2).
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// bounded: a protocol error traps (launch failure) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_b(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (long spin = 0; spin < (1L << 28); ++spin) {
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+        if (done) return;
+    }
+    __trap();
+}
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
+}
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
+    gemm_tc_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                 const __grid_constant__ EpiParams ep) {
+    constexpr int BN = 256;
+    using S = SmemP<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::n_bars);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = int(cluster_rank());
+    const int cid = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
+    const int mt = (M + BM - 1) / BM, mt2 = (mt + 1) / 2, nt = N / BN, units = mt2 * nt;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 2);  // both CTAs' MMAs must be done with the stage
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull0 + 8 * i, 1);
+            mbar_init(tempty0 + 8 * i, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // the peer's barriers are initialised before any multicast lands in them
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: own A tile + half of the pair's B tile, multicast
+            int it = 0;
+            for (int u = cid; u < units; u += n_cl) {
+                const int m0 = (2 * (u % mt2) + rank) * BM, n0 = (u / mt2) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait_b(empty0 + 8 * st, ((it / STAGES) & 1) ^ 1);
+                    const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+                    mbar_expect_tx(full0 + 8 * st, S::stage_bytes);
+                    tma_load_2d(sa, &tmA, full0 + 8 * st, kb * BK, m0);
+                    tma_load_2d_mc(sa + S::a_bytes + rank * (S::b_bytes / 2), &tmB, full0 + 8 * st, kb * BK, n0 + rank * (BN / 2),
+                                   uint16_t(3));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer (this CTA's 128 rows)
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            int it = 0, local = 0;
+            for (int u = cid; u < units; u += n_cl, ++local) {
+                const int acc = local & 1;
+                mbar_wait_b(tempty0 + 8 * acc, ((local >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(acc * BN);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait_b(full0 + 8 * st, (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + st * S::stage_bytes);
+                    const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + S::a_bytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) tc_mma(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    tc_commit_mc(empty0 + 8 * st, uint16_t(3));  // frees the slot in both CTAs
+                }
+                tc_commit(tfull0 + 8 * acc);
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        int local = 0;
+        for (int u = cid; u < units; u += n_cl, ++local) {
+            const int acc = local & 1;
+            const int m0 = (2 * (u % mt2) + rank) * BM, n0 = (u / mt2) * BN;
+            mbar_wait_b(tfull0 + 8 * acc, (local >> 1) & 1);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
+                if (m < M) epilogue32(ep, m, n0 + c, v);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+}
+
+// ------------------------------------------------------------------ CTA-pair UMMA kernel (cta_group::2)
+// The Blackwell 2-SM GEMM: a cluster of two CTAs on one TPC computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256) issued by the leader. Each CTA TMA-loads its own 128 rows of
+// A and its own 128 rows (N half) of B into its own smem; the MMA reads A from both SMs and B from
+// both SMs, and each SM's TMEM receives its 128 accumulator rows. Per SM and 64-deep K step that is
+// 32 KB of TMA writes + 32 KB of MMA reads of shared memory instead of 48 + 48 KB — the single-CTA
+// 128 x 256 tile needs 188 B/clk of smem bandwidth at full MMA rate, more than the SM has.
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit2_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
+}
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
+    gemm_tc_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                const __grid_constant__ EpiParams ep) {
+    constexpr int BN = 256;                 // pair tile 256 x 256; each CTA holds 128 rows of A and of B
+    constexpr int a_bytes = BM * BK * 2, b_bytes = 128 * BK * 2, stage_bytes = a_bytes + b_bytes;  // 32 KB
+    constexpr int bars_off = STAGES * stage_bytes;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bars_off);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
+    const int mt = (M + BM - 1) / BM, mt2 = (mt + 1) / 2, nt = N / BN, units = mt2 * nt;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full0 + 8 * i, 2);   // leader's: one expect_tx arrive per CTA
+            mbar_init(empty0 + 8 * i, 1);  // each CTA's: the leader's multicast commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull0 + 8 * i, 1);
+            mbar_init(tempty0 + 8 * i, 8);  // leader's: 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 2) {  // pair allocation: the same columns in both SMs' TMEM
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs): own A rows + own B half, signalling the leader
+            int it = 0;
+            for (int u = cid; u < units; u += n_cl) {
+                const int m0 = (2 * (u % mt2) + int(rank)) * BM, n0 = (u / mt2) * BN + int(rank) * 128;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait_b(empty0 + 8 * st, ((it / STAGES) & 1) ^ 1);
+                    const uint32_t sa = smem_u32(smem + st * stage_bytes);
+                    const uint32_t fb = map_to_rank(full0 + 8 * st, 0);
+                    mbar_arrive_expect_tx_cluster(fb, stage_bytes);
+                    tma_load_2d_2sm(sa, &tmA, fb, kb * BK, m0);
+                    tma_load_2d_2sm(sa + a_bytes, &tmB, fb, kb * BK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {  // ---- MMA issuer: M = 256 across the pair
+            constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+            int it = 0, local = 0;
+            for (int u = cid; u < units; u += n_cl, ++local) {
+                const int acc = local & 1;
+                mbar_wait_b(tempty0 + 8 * acc, ((local >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(acc * BN);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    mbar_wait_b(full0 + 8 * st, (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + st * stage_bytes);
+                    const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + a_bytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) tc_mma2(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    tc_commit2_mc(empty0 + 8 * st, uint16_t(3));
+                }
+                tc_commit2_mc(tfull0 + 8 * acc, uint16_t(3));
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const uint32_t te_leader = map_to_rank(tempty0, 0);
+        int local = 0;
+        for (int u = cid; u < units; u += n_cl, ++local) {
+            const int acc = local & 1;
+            const int m0 = (2 * (u % mt2) + int(rank)) * BM, n0 = (u / mt2) * BN;
+            mbar_wait_b(tfull0 + 8 * acc, (local >> 1) & 1);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+            for (int c = 0; c < BN; c += 32) {
+                float v[32];
+                tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
+                if (m < M) epilogue32(ep, m, n0 + c, v);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(te_leader + 8 * acc);
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+}
+
 // ------------------------------------------------------------------ SIMT reference
 __global__ void gemm_simt_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B, int M, int N,
                                  int K, EpiParams ep) {
@@ -496,11 +787,57 @@ void launch_persistent(const void* A, const void* B, int M, int N, int K, const 
 
 }  // namespace
 
+template <int STAGES>
+void launch_pair(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    using S = SmemP<256, STAGES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_pair<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::total));
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map_2d(A, M, K, BM);
+    const CUtensorMap tb = make_map_2d(B, N, K, 128);  // half of a 256-column B tile per CTA
+    const int units = (((M + BM - 1) / BM + 1) / 2) * (N / 256);
+    const int grid = 2 * std::max(1, std::min(units, sm_count() / 2));
+    gemm_tc_pair<STAGES><<<grid, kPersistThreads, S::total, s>>>(ta, tb, M, N, K, ep);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
+template <int STAGES>
+void launch_2sm(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
+    constexpr int total = STAGES * (BM * BK * 2 + 128 * BK * 2) + (2 * STAGES + 4) * 8 + 16 + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_2sm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, total));
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map_2d(A, M, K, BM);
+    const CUtensorMap tb = make_map_2d(B, N, K, 128);
+    const int units = (((M + BM - 1) / BM + 1) / 2) * (N / 256);
+    const int grid = 2 * std::max(1, std::min(units, sm_count() / 2));
+    gemm_tc_2sm<STAGES><<<grid, kPersistThreads, total, s>>>(ta, tb, M, N, K, ep);
+    TKV_CUDA_CHECK(cudaGetLastError());
+}
+
+int gemm_mode() {  // TKV_GEMM = single | pair | 2sm (A/B measurements); default single
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = std::getenv("TKV_GEMM");
+        const std::string v = e ? e : "";
+        mode = v == "pair" ? 1 : v == "2sm" ? 2 : 0;
+    }
+    return mode;
+}
+
 void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     if (M == 0) return;
     if (K % 8 || N % 32) throw std::invalid_argument("gemm_bf16: need K % 8 == 0 and N % 32 == 0");
     // persistent warp-specialised kernel; 128x256 tiles when N allows, else 128x128 with a deeper ring
-    if (N % 256 == 0)
+    if (N % 256 == 0 && M > 128 && gemm_mode() == 2)
+        launch_2sm<6>(A, B, M, N, K, ep, s);
+    else if (N % 256 == 0 && M > 128 && gemm_mode() == 1)
+        launch_pair<4>(A, B, M, N, K, ep, s);
+    else if (N % 256 == 0)
         launch_persistent<256, 4>(A, B, M, N, K, ep, s);
     else
         launch_persistent<128, 6>(A, B, M, N, K, ep, s);

@@ -103,22 +103,37 @@ std::vector<size_t> rerank_device(const uint64_t* inc, size_t n, size_t words, u
         }
         std::vector<uint64_t> packed(m * words);
         for (size_t k = 0; k < m; ++k) std::copy(inc + live[k] * words, inc + (live[k] + 1) * words, packed.begin() + long(k * words));
-        uint64_t* d_inc = nullptr;
-        int32_t* d_order = nullptr;
-        TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_inc), std::max<size_t>(8, packed.size() * 8), s));
-        TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_order), m * 4, s));
-        TKV_CUDA_CHECK(cudaMemcpyAsync(d_inc, packed.data(), packed.size() * 8, cudaMemcpyHostToDevice, s));
+        // per-thread device scratch, grown on demand and kept (no allocator traffic per batch)
+        struct Scratch {
+            int device = -1;
+            uint64_t* inc = nullptr;
+            int32_t* order = nullptr;
+            size_t cap = 0;
+        };
+        static thread_local Scratch sc;
+        int dev = 0;
+        TKV_CUDA_CHECK(cudaGetDevice(&dev));
+        if (sc.device != dev || sc.cap < m * (words + 1)) {
+            if (sc.device == dev) {
+                cudaFree(sc.inc);
+                cudaFree(sc.order);
+            }
+            sc.device = dev;
+            sc.cap = std::max<size_t>(m * (words + 1), 1 << 16);
+            TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.inc), sc.cap * 8));
+            TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.order), sc.cap * 4));
+            TKV_CUDA_CHECK(cudaFuncSetAttribute(rerank_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096));
+        }
+        TKV_CUDA_CHECK(cudaMemcpyAsync(sc.inc, packed.data(), packed.size() * 8, cudaMemcpyHostToDevice, s));
         const size_t base = (kMaxWords + size_t(used_u64(int(m))) + 32) * 8;
         const size_t full = base + packed.size() * 8;
         const bool in_smem = full <= 200 * 1024;
         const size_t smem = in_smem ? full : base;
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(rerank_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        rerank_chain_kernel<<<1, kThreads, smem, s>>>(d_inc, int(m), int(words), int(first), int(in_smem), d_order);
+        if (smem > 200 * 1024 + 4096) throw std::invalid_argument("device rerank: batch too large for one CTA's bitmask");
+        rerank_chain_kernel<<<1, kThreads, smem, s>>>(sc.inc, int(m), int(words), int(first), int(in_smem), sc.order);
         TKV_CUDA_CHECK(cudaGetLastError());
         std::vector<int32_t> ord(m);
-        TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), d_order, m * 4, cudaMemcpyDeviceToHost, s));
-        TKV_CUDA_CHECK(cudaFreeAsync(d_inc, s));
-        TKV_CUDA_CHECK(cudaFreeAsync(d_order, s));
+        TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), sc.order, m * 4, cudaMemcpyDeviceToHost, s));
         TKV_CUDA_CHECK(cudaStreamSynchronize(s));
         for (int32_t k : ord) out.push_back(live[size_t(k)]);
     }
