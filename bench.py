@@ -384,7 +384,9 @@ def main():
         "global_rerank_ms_per_step": sum(timed_rerank_ms) / args.steps,
         "attention_ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
         "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,
-                "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5)},
+                "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5),
+                "last_step_ms": {"prompt_analysis": e2e_res.get("analyze_ms"), "host_enqueue": e2e_res["host_ms"],
+                                 "device_makespan": e2e_res["makespan_ms"]}},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -973,7 +974,8 @@ void tkv_serve_options_default(tkv_serve_options* o) {
 }
 
 namespace {
-int serve_impl(tkv_store* s, std::vector<tkv::ServeQuery>& qs, const tkv_serve_options* o, float* logits_out, char** result_json) {
+int serve_impl(tkv_store* s, std::vector<tkv::ServeQuery>& qs, const tkv_serve_options* o, float* logits_out, char** result_json,
+               double analyze_ms = 0) {
     return guard([&] {
         need(s && o, "null argument");
         set_device(s->model->device);
@@ -981,7 +983,11 @@ int serve_impl(tkv_store* s, std::vector<tkv::ServeQuery>& qs, const tkv_serve_o
         so.keep_logits = logits_out != nullptr;
         tkv::ServeResult R = o->nocache ? s->server->serve_nocache(qs, so) : s->server->serve(qs, so);
         if (logits_out && !R.logits.empty()) std::memcpy(logits_out, R.logits.data(), R.logits.size() * 4);
-        if (result_json) *result_json = dup_string(serve_result_json(R).dump());
+        if (result_json) {
+            json j = serve_result_json(R);
+            j["analyze_ms"] = analyze_ms;  // prompt text -> tables + suffix on the host (tkv_serve_text)
+            *result_json = dup_string(j.dump());
+        }
     });
 }
 }  // namespace
@@ -1004,6 +1010,7 @@ int tkv_serve(tkv_store* s, size_t n, const int64_t* table_off, const int32_t* t
 int tkv_serve_text(tkv_store* s, const tkv_engine* e, size_t n, const char* const* ids, const char* const* texts,
                    const tkv_serve_options* o, float* logits_out, char** result_json) {
     std::vector<tkv::ServeQuery> qs(n);
+    const auto t_an = std::chrono::steady_clock::now();
     const int rc = guard([&] {
         need(e && texts, "null argument");
         // prompt analysis (tokenize -> Table Trie -> assembly order) is pure per prompt and the trie
@@ -1031,7 +1038,8 @@ int tkv_serve_text(tkv_store* s, const tkv_engine* e, size_t n, const char* cons
             if (ep) std::rethrow_exception(ep);
     });
     if (rc != TKV_OK) return rc;
-    return serve_impl(s, qs, o, logits_out, result_json);
+    const double an_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_an).count();
+    return serve_impl(s, qs, o, logits_out, result_json, an_ms);
 }
 
 // ------------------------------------------------------------------ measurement

@@ -5,6 +5,8 @@
 // compute), evicted tables' pages are recycled only after the compute that may read them.
 // Each window of b_c queries is one gather + one batched prefill on the compute stream.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -182,6 +184,13 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     std::vector<std::vector<int>> qt;
     std::vector<int> qn;
     for (const auto& q : queries) qt.push_back(q.tables), qn.push_back(int(q.suffix.size()));
+    static const bool host_prof = std::getenv("TKV_HOST_PROFILE") != nullptr;  // debug: host-side phase timers
+    double hp_plan = 0, hp_copy = 0, hp_fwd = 0, hp_rest = 0, hp_mark = now_ms();
+    auto hp_tick = [&](double& acc) {
+        const double t = now_ms();
+        acc += t - hp_mark;
+        hp_mark = t;
+    };
     BatchTrace bt = plan_batch(qt, qn, opts, arena_, cs_);
     R.order = std::move(bt.order);
     const tablekv::BatchPlan& plan = bt.plan;
@@ -308,6 +317,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     R.window_of.assign(plan.queries.size(), 0);
     R.argmax.assign(plan.queries.size(), -1);
 
+    hp_tick(hp_plan);
     for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
         const auto& w = plan.windows[wi];
         const auto& wt = tr.windows[wi];
@@ -373,6 +383,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 for (auto& kv : local) dropped.push_back({-1, std::move(kv.second)});
         }
         cudaEvent_t d0 = evp.get(), p0 = evp.get(), d1 = evp.get(), p1 = evp.get();
+        hp_tick(hp_rest);
         TKV_CUDA_CHECK(cudaEventRecord(d0, ds_));
         flush_copies(ds_);
         TKV_CUDA_CHECK(cudaEventRecord(d1, ds_));
@@ -381,6 +392,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         TKV_CUDA_CHECK(cudaEventRecord(p1, ps_));
         dspan.push_back({d0, d1});
         pspan.push_back({p0, p1});
+        hp_tick(hp_copy);
         cudaEvent_t x1 = nullptr;
         if (peering) {
             // peer copies of window w run during compute(w-1): the peers are then around the
@@ -511,9 +523,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             fa.logits_out = d_logits;
             fa.argmax_out = d_argmax + w.begin;  // compacted per window; remapped below
             R.meta_bytes += tokens.size() * 16 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
+            hp_tick(hp_rest);
             model_.set_timing(opts.time_kernels);
             model_.forward(fa, cs_);
             R.launches += model_.launches();
+            hp_tick(hp_fwd);
             if (opts.keep_logits) {
                 for (size_t k = 0; k < seq_query.size(); ++k)
                     TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
@@ -540,6 +554,10 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     for (auto& kv : resident) pool_.release(kv.second, cs_);
     resident.clear();
     R.host_ms = now_ms() - host0;
+    hp_tick(hp_rest);
+    if (host_prof)
+        std::fprintf(stderr, "[tkv host] plan %.1f ms, copies %.1f ms, forward enqueue %.1f ms, rest %.1f ms (windows %zu)\n",
+                     hp_plan, hp_copy, hp_fwd, hp_rest, plan.windows.size());
     TKV_CUDA_CHECK(cudaStreamSynchronize(ps_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(ds_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(xs_));
