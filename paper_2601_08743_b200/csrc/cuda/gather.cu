@@ -9,6 +9,8 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 namespace tkv {
@@ -172,12 +174,108 @@ __global__ void __launch_bounds__(256) gather_rope_bf16_kernel(const uint8_t* __
     }
 }
 
+// TMA-staged variant: CTA = up to kTmaRows rows of one table segment for one layer. One thread
+// moves the rows' K and V bytes (contiguous runs of the table image, split only at page
+// boundaries) into shared memory with cp.async.bulk, all threads rotate K in place, then bulk
+// stores write both runs into the slab — the loads/stores are a handful of bulk copies per CTA
+// instead of 16-byte LSU traffic.
+constexpr int kTmaRows = 16;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst), "l"(src),
+                 "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(256) gather_rope_tma_kernel(const uint8_t* __restrict__ pool, int page_shift,
+                                                              const int32_t* __restrict__ page_ids,
+                                                              const GatherSeg* __restrict__ segs, const int4* __restrict__ chunks,
+                                                              int L, int l, int kvdim, int head_dim,
+                                                              const float* __restrict__ cos_f, const float* __restrict__ sin_f,
+                                                              uint8_t* __restrict__ out_k, uint8_t* __restrict__ out_v) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const int4 ch = chunks[blockIdx.x];  // {seg, t0, rows, 0}
+    const GatherSeg sg = segs[ch.x];
+    const long row_bytes = long(kvdim) * 2;
+    const uint32_t run = uint32_t(ch.z * row_bytes);
+    const uint32_t s_k = uint32_t(__cvta_generic_to_shared(sm)), s_v = s_k + run;
+    const uint32_t b = uint32_t(__cvta_generic_to_shared(&bar));
+    const long pmask = (1L << page_shift) - 1;
+    const int32_t* pages = page_ids + sg.page_off;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * run) : "memory");
+        for (int kv = 0; kv < 2; ++kv) {
+            long off = ((long(kv) * L + l) * sg.tokens + ch.y) * row_bytes;
+            uint32_t dst = kv ? s_v : s_k, left = run;
+            while (left) {  // split the run at page boundaries
+                const long room = (1L << page_shift) - (off & pmask);
+                const uint32_t n = uint32_t(long(left) < room ? long(left) : room);
+                bulk_g2s(dst, pool + (long(pages[off >> page_shift]) << page_shift) + (off & pmask), n, b);
+                off += n, dst += n, left -= n;
+            }
+        }
+    }
+    __syncthreads();
+    {  // wait for both runs
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(done)
+                         : "r"(b)
+                         : "memory");
+    }
+    const int vpr = kvdim >> 3, half = head_dim >> 1;
+    for (int i = threadIdx.x; i < ch.z * vpr; i += blockDim.x) {
+        const int r = i / vpr, vi = i - r * vpr;
+        const long pos = sg.pos0 + ch.y + r;
+        if (pos == 0) continue;
+        uint4* p = reinterpret_cast<uint4*>(sm + long(r) * row_bytes + vi * 16);
+        uint4 w = *p;
+        const int k0 = ((vi * 8) % head_dim) >> 1;
+        const float4 c = *reinterpret_cast<const float4*>(cos_f + pos * half + k0);
+        const float4 sn = *reinterpret_cast<const float4*>(sin_f + pos * half + k0);
+        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+        const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 ab = unpack_bf16x2(wp[e]);
+            wp[e] = pack_bf16x2(fmaf(ab.x, cc[e], -ab.y * ss[e]), fmaf(ab.x, ss[e], ab.y * cc[e]));
+        }
+        *p = w;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> bulk store reads
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const long o = long(sg.out_row0 + ch.y) * row_bytes;
+        bulk_s2g(out_k + o, s_k, run);
+        bulk_s2g(out_v + o, s_v, run);
+        asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+}
+
 }  // namespace
+
+bool gather_use_tma() {  // TKV_GATHER=lsu selects the 16-byte LSU kernel (A/B measurements)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("TKV_GATHER");
+        v = (e && std::string(e) == "lsu") ? 0 : 1;
+    }
+    return v == 1;
+}
 
 int gather_chunks(const GatherSeg* segs, int n_segs, std::vector<int4>& out) {
     out.clear();
+    const int rows = gather_use_tma() ? kTmaRows : kChunkRows;
     for (int s = 0; s < n_segs; ++s)
-        for (int t = 0; t < segs[s].tokens; t += kChunkRows) out.push_back(make_int4(s, t, std::min(kChunkRows, segs[s].tokens - t), 0));
+        for (int t = 0; t < segs[s].tokens; t += rows) out.push_back(make_int4(s, t, std::min(rows, segs[s].tokens - t), 0));
     return int(out.size());
 }
 
@@ -189,9 +287,20 @@ void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32
     if (page_bytes & (page_bytes - 1)) throw std::invalid_argument("gather fast path: page size must be a power of two");
     int shift = 0;
     while ((size_t(1) << shift) < page_bytes) ++shift;
-    gather_rope_bf16_kernel<<<n_chunks, 32 * kChunkRows, 0, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim,
-                                                                 head_dim, cos_f, sin_f, static_cast<uint8_t*>(out_k),
-                                                                 static_cast<uint8_t*>(out_v));
+    if (gather_use_tma()) {
+        const int smem = 2 * kTmaRows * kvdim * 2;
+        static bool attr = false;
+        if (!attr) {
+            TKV_CUDA_CHECK(cudaFuncSetAttribute(gather_rope_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = true;
+        }
+        gather_rope_tma_kernel<<<n_chunks, 256, smem, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim, head_dim,
+                                                           cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v));
+    } else {
+        gather_rope_bf16_kernel<<<n_chunks, 32 * kChunkRows, 0, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim,
+                                                                     head_dim, cos_f, sin_f, static_cast<uint8_t*>(out_k),
+                                                                     static_cast<uint8_t*>(out_v));
+    }
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 
