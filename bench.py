@@ -120,8 +120,8 @@ def reference_arm(args, rank, world):
     per_q = []
     walls = []
     for step in range(args.warmup + args.steps):
-        out = subprocess.run([exe, "wide", "32", "128", str(threads)] + samples, capture_output=True, text=True,
-                             check=True)
+        out = subprocess.run([exe, "wide", "32", "128", str(threads), "--cached-only"] + samples, capture_output=True,
+                             text=True, check=True)
         r = json.loads(out.stdout)
         if step >= args.warmup:
             per_q += [c * L for c in r["cached_s"]]
@@ -153,7 +153,8 @@ def cpu_baseline_sample(eng, entries, n=4):
         a = eng.analyze(text)
         nctx = sum(len(eng.info["table_tokens"][t]) for t in a["assembly_order"])
         samples.append("%d:%d" % (nctx, len(a["remainder"])))
-    out = subprocess.run([exe, "wide", "32", "128", str(threads)] + samples, capture_output=True, text=True, check=True)
+    out = subprocess.run([exe, "wide", "32", "128", str(threads), "--cached-only"] + samples, capture_output=True, text=True,
+                         check=True)
     r = json.loads(out.stdout)
     L = LLAMA8B["num_layers"]
     qps = len(samples) / (r["cached_wall_s"] * L)

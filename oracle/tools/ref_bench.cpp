@@ -10,7 +10,7 @@
 //       proj/src/engine.cpp:174-205 minus the oracle) and the no-cache block-masked
 //       prefill over the same layout. Queries are sharded over <threads> threads
 //       (the attention functions are pure).
-//   ref_bench wide <heads> <head_dim> <threads> <nctx:nq>...
+//   ref_bench wide <heads> <head_dim> <threads> [--cached-only] <nctx:nq>...
 //       ONE layer of the reference architecture at the given width (MHA, LN, SiLU 4h),
 //       per sample: query_attend of nq tokens over an nctx-token assembled context,
 //       and the no-cache prefill of nctx+nq tokens. The caller scales by layer count.
@@ -118,8 +118,13 @@ int cmd_wide(int argc, char** argv) {
     const int threads = std::stoi(argv[4]);
     struct Sample { int nctx, nq; };
     std::vector<Sample> samples;
+    bool cached_only = false;  // --cached-only: skip the no-cache prefill (the reference arm's metric is the cached path)
     for (int a = 5; a < argc; ++a) {
         std::string s = argv[a];
+        if (s == "--cached-only") {
+            cached_only = true;
+            continue;
+        }
         const auto c = s.find(':');
         samples.push_back({std::stoi(s.substr(0, c)), std::stoi(s.substr(c + 1))});
     }
@@ -146,7 +151,7 @@ int cmd_wide(int argc, char** argv) {
         cached[i] = now() - t0;
         (void)h;
     });
-    const double wall_nocache = run_sharded(n, threads, [&](int i) {
+    const double wall_nocache = cached_only ? 0.0 : run_sharded(n, threads, [&](int i) {
         BlockMask mask;
         mask.append_block(0, samples[i].nctx);
         mask.append_block(kQueryGroup, samples[i].nq);
