@@ -20,6 +20,8 @@ struct AttnArgs {
     __nv_bfloat16* out;          // [M][Hq*d]
     int num_heads, kv_heads, head_dim, mode;
     float scale;                 // 1/sqrt(d)
+    const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row
+                                      // (start of the row's group block; 0 for query rows)
 };
 
 // tokens per CTA tile for a GQA ratio (rows per CTA / G)

@@ -15,8 +15,9 @@
 // Warpgroups 1 / 2 (warps 4-7 / 8-11, registers raised with setmaxnreg): softmax of stream 0 / 1 — TMEM lane = query row, each thread owns one row:
 // loads its 128 S values, row max, conditional rescale of O in TMEM (only when the max grows by
 // more than 2^8), P = exp2(S*scale*log2e - m) packed to bf16 and stored over S's columns.
-// Mask: own rows see every cached prefix row + causal own (query_attend, attention.hpp:368-414);
-// the block-causal prefill mask runs on attn_tc.cu.
+// Masks: mode 0 — own rows see every cached prefix row + causal own (query_attend,
+// attention.hpp:368-414); mode 1 — block-causal prefill over contiguous group blocks (prefill /
+// encode_group, attention.hpp:210-294): a row sees [its group block's first row, itself].
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -388,6 +389,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool live = tok_local < it.n_tok;
             const int tok = it.tok0 + min(tok_local, it.n_tok - 1);
             const int causal = sq.n_ctx + tok;  // last visible combined key index
+            // block-causal prefill (BlockMask::allows, attention.hpp:37-39) with contiguous group
+            // blocks: a row sees own keys [first key of its group block, itself]
+            const int lo = a.mode == 1 ? a.row_lo[sq.q_row0 + tok] : 0;
             float m_run = -INFINITY, l_run = 0.f;
             for (int t = 0; t < it.n_tiles; ++t) {
                 const long gi = g + t;
@@ -406,10 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < BN; ++c) mx = fmaxf(mx, __uint_as_float(u[c]));
                 } else {
-                    const int lim = min(seg_end, causal + 1) - base_j;  // columns [0, lim) visible
+                    const int lim = min(seg_end, causal + 1) - base_j;  // columns [lo_c, lim) visible
+                    const int lo_c = lo - base_j;
 #pragma unroll
                     for (int c = 0; c < BN; ++c) {
-                        if (c >= lim) u[c] = 0xff800000u;  // -inf
+                        if (c >= lim || c < lo_c) u[c] = 0xff800000u;  // -inf
                         mx = fmaxf(mx, __uint_as_float(u[c]));
                     }
                 }
@@ -534,7 +539,7 @@ int attn_tc5_rows_per_tile(int num_heads, int kv_heads) { return 2 * BM / (num_h
 void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_rows, long own_rows, cudaStream_t s) {
     if (n_work == 0) return;
     if (!attention_tc5_supported(a)) throw std::invalid_argument("tcgen05 attention needs head_dim 128");
-    if (a.mode != 0) throw std::invalid_argument("tcgen05 attention serves the cached-prefix mask (mode 0)");
+    if (a.mode == 1 && !a.row_lo) throw std::invalid_argument("tcgen05 block-mask attention needs per-row group starts");
     static bool attr = false;
     if (!attr) {
         TKV_CUDA_CHECK(cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));

@@ -45,6 +45,7 @@ void forward_host(Model& model, cudaStream_t s, const HostFwd& h) {
     a.pos = static_cast<const int32_t*>(up(pos.data(), size_t(h.n) * 4));
     a.pos64 = static_cast<const int64_t*>(up(pos64.data(), size_t(h.n) * 8));
     if (h.groups) a.group = static_cast<const int32_t*>(up(h.groups, size_t(h.n) * 4));
+    a.group_host = h.groups;
     const AttnSeq seq{0, h.n, 0, h.mode == 0 ? h.n_ctx : 0};
     a.n_seqs = 1;
     a.seqs = static_cast<const AttnSeq*>(up(&seq, sizeof(seq)));

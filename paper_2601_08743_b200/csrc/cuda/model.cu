@@ -238,7 +238,32 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
     // mma.sync kernel for other head dims and for block-mask prefill (mode 1: its per-key group
     // test runs cheaper there)
     const int G = c.num_heads / c.kv_heads;
-    const bool use_tc5 = attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0 && a.mode == 0;
+    // block-causal prefill (mode 1) runs on the tcgen05 kernel when every sequence's group ids form
+    // contiguous blocks (the prompt layout of prefill / encode_group): row i then sees own keys
+    // [start of its block, i], or [0, i] for query rows (group -1)
+    const int32_t* d_row_lo = nullptr;
+    if (a.mode == 1 && a.group_host && attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0) {
+        std::vector<int32_t> lo(static_cast<size_t>(M), 0);
+        bool contiguous = true;
+        for (int si = 0; si < a.n_seqs && contiguous; ++si) {
+            const AttnSeq& q = a.seqs_host[si];
+            std::vector<int32_t> seen;
+            int start = 0;
+            for (int i = 0; i < q.n_own; ++i) {
+                const int32_t g = a.group_host[q.q_row0 + i];
+                if (i == 0 || g != a.group_host[q.q_row0 + i - 1]) {
+                    start = i;
+                    if (g != -1) {
+                        if (std::find(seen.begin(), seen.end(), g) != seen.end()) contiguous = false;
+                        seen.push_back(g);
+                    }
+                }
+                lo[size_t(q.q_row0 + i)] = g == -1 ? 0 : start;
+            }
+        }
+        if (contiguous) d_row_lo = static_cast<const int32_t*>(ring_.upload(lo.data(), lo.size() * 4, s));
+    }
+    const bool use_tc5 = attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0 && (a.mode == 0 || d_row_lo != nullptr);
     const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
@@ -328,6 +353,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.head_dim = c.head_dim;
         aa.mode = a.mode;
         aa.scale = float(1.0 / std::sqrt(double(c.head_dim)));
+        aa.row_lo = d_row_lo;
         {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing_) {

@@ -69,6 +69,7 @@ struct FwdArgs {
     const int32_t* pos = nullptr;       // device [M] global positions
     const int64_t* pos64 = nullptr;     // device [M] (reference-precision path)
     const int32_t* group = nullptr;     // device [M] (mode 1)
+    const int32_t* group_host = nullptr;  // host copy (mode 1 on the tcgen05 attention)
     int n_seqs = 0;
     const AttnSeq* seqs = nullptr;      // device
     const AttnSeq* seqs_host = nullptr; // host copy (tile planning)

@@ -681,6 +681,7 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
                 fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
                 fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
                 fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
+                fa.group_host = group.data();
                 fa.n_seqs = int(seqs.size());
                 fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
                 fa.seqs_host = seqs.data();
