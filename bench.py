@@ -321,7 +321,9 @@ def main():
     barrier()
     te = time.perf_counter()
     for _ in range(args.steps):  # prompt text in (host analysis, H2D), first tokens out (D2H), per step
+        tc = time.perf_counter()
         e2e_res = store.serve_text(eng, e2e_texts, options=e2e_opts)
+        e2e_last_wall = time.perf_counter() - tc
     e2e_s = (time.perf_counter() - te) / args.steps
     if world > 1:
         t = torch.tensor([e2e_s], device=coll_dev)
@@ -387,7 +389,8 @@ def main():
         "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5),
                 "last_step_ms": {"prompt_analysis": e2e_res.get("analyze_ms"), "host_enqueue": e2e_res["host_ms"],
-                                 "device_makespan": e2e_res["makespan_ms"]}},
+                                 "device_makespan": e2e_res["makespan_ms"], "serve_wall": e2e_res["wall_ms"],
+                                 "call_wall": e2e_last_wall * 1e3}},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

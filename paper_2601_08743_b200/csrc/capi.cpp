@@ -187,6 +187,7 @@ json serve_result_json(const tkv::ServeResult& R) {
             {"copy_demand_ms", R.copy_demand_ms},
             {"makespan_ms", R.makespan_ms},
             {"host_ms", R.host_ms},
+            {"wall_ms", R.wall_ms},
             {"launches", R.launches},
             {"gemm_ms", R.gemm_ms},
             {"gemm_flops", R.gemm_flops},

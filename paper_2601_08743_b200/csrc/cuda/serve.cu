@@ -586,6 +586,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     if (opts.keep_logits) R.logits = std::move(logits_host);
     TKV_CUDA_CHECK(cudaFree(d_argmax));
     TKV_CUDA_CHECK(cudaFree(d_logits));
+    R.wall_ms = now_ms() - host0;
     return R;
 }
 

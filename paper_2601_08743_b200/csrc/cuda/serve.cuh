@@ -66,6 +66,7 @@ struct ServeResult {
     double copy_busy_ms = 0;               // sum of per-window copy spans (both copy streams)
     double copy_demand_ms = 0;             // demand stream only (its copies run back to back)
     double makespan_ms = 0, host_ms = 0;
+    double wall_ms = 0;                    // serve() entry to return on the host clock
     long launches = 0;
     double gemm_ms = 0, gemm_flops = 0;    // time_kernels only
     double gather_ms = 0, gather_bytes = 0;
