@@ -369,3 +369,31 @@ def test_load_dir_reference_and_bf16_images(tmp_path, f32_store):
     a.close()
     b.close()
     mb.close()
+
+
+@pytest.mark.parametrize("run_name", ["lru", "fifo", "lfu", "lru_nopipe", "lru_small"])
+def test_executor_replays_c2_reference_traces(run_name):
+    """The GPU executor at the C2 scale (1000 queries, 200 tables; the reference's own run_batch
+    over the same records is the golden): served order, per-record hit/miss/evict sequence,
+    counters and loaded bytes are bit-exact; arena bytes are random (the trace does not read them)."""
+    g = load("c2")["result"]
+    run = next(r for r in GI.c2_runs() if r["name"] == run_name)
+    ref = g["runs"][run_name]
+    m = N.Model(dtype="f32", num_layers=2, num_heads=4, head_dim=16, vocab_size=g["vocab_size"])
+    s = N.Store(m, page_bytes=64 << 10, n_pages=4096)
+    rng = np.random.default_rng(5)
+    sizes = {}
+    for t, toks in enumerate(g["table_tokens"]):
+        payload = rng.standard_normal(2 * 2 * len(toks) * 64).astype(np.float32) * 0.1
+        s.put(t, len(toks), 0, payload, "f32")
+        sizes[t] = payload.nbytes
+    qs = [(q["assembly_order"], q["remainder"]) for q in g["queries"]]
+    res = s.serve(qs, rerank_on=int(run["rerank_on"]), pipeline_on=int(run["pipeline_on"]), capacity=run["capacity"],
+                  policy=run["policy"], b_c=run["b_c"], b_m=run["b_m"], seed=run["seed"])
+    assert res["order"] == ref["order"]
+    assert [t[:6] for t in res["trace"]] == _trace_from_golden(ref)
+    assert res["counters"] == [ref["trace_counters"][k] for k in ("hits", "misses", "swaps", "prefetch_loads")]
+    assert res["h2d_bytes"] == sum(sizes[t[3]] for t in res["trace"] if t[5])
+    assert s.info()["free_pages"] == 4096
+    s.close()
+    m.close()
