@@ -30,9 +30,6 @@ struct PageList {
 // coalesced 16-byte loads/stores (the north-star "vectorised H2D"); bytes % 16 == 0.
 void launch_h2d_pages(const void* src_mapped, size_t bytes, uint8_t* pool, size_t page_bytes, const PageList& pages,
                       int n_ctas, cudaStream_t s);
-// Device-to-device variant (peer pool pointer or local), same page addressing on both sides.
-void launch_d2d_pages(const uint8_t* src_pool, size_t src_page_bytes, const PageList& src_pages, uint8_t* dst_pool,
-                      size_t dst_page_bytes, const PageList& dst_pages, size_t bytes, cudaStream_t s);
 
 // ---- gather.cu: assemble (proj/include/tablekv/attention.hpp:300-362) ----------------------
 struct GatherSeg {

@@ -44,15 +44,6 @@ __global__ void h2d_pages_kernel(const uint4* __restrict__ src, long n_vec, uint
     }
 }
 
-__global__ void d2d_pages_kernel(const uint8_t* __restrict__ src_pool, long src_page_vecs, PageList src_pages,
-                                 uint8_t* __restrict__ dst_pool, long dst_page_vecs, PageList dst_pages, long n_vec) {
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n_vec; i += long(gridDim.x) * blockDim.x) {
-        const long sp = i / src_page_vecs, dp = i / dst_page_vecs;
-        const uint4 v = reinterpret_cast<const uint4*>(src_pool)[long(src_pages.page[sp]) * src_page_vecs + (i - sp * src_page_vecs)];
-        reinterpret_cast<uint4*>(dst_pool)[long(dst_pages.page[dp]) * dst_page_vecs + (i - dp * dst_page_vecs)] = v;
-    }
-}
-
 }  // namespace
 
 void launch_h2d_pages(const void* src_mapped, size_t bytes, uint8_t* pool, size_t page_bytes, const PageList& pages,
@@ -64,16 +55,6 @@ void launch_h2d_pages(const void* src_mapped, size_t bytes, uint8_t* pool, size_
     const int blocks = std::max(1, std::min(n_ctas, ceil_div(n_vec, threads)));
     h2d_pages_kernel<<<blocks, threads, 0, s>>>(static_cast<const uint4*>(src_mapped), n_vec, pool,
                                                 long(page_bytes / 16), pages);
-    TKV_CUDA_CHECK(cudaGetLastError());
-}
-
-void launch_d2d_pages(const uint8_t* src_pool, size_t src_page_bytes, const PageList& src_pages, uint8_t* dst_pool,
-                      size_t dst_page_bytes, const PageList& dst_pages, size_t bytes, cudaStream_t s) {
-    if (bytes == 0) return;
-    const long n_vec = long(bytes / 16);
-    const int blocks = std::min(kNumSMs * 2, ceil_div(n_vec, 512));
-    d2d_pages_kernel<<<blocks, 512, 0, s>>>(src_pool, long(src_page_bytes / 16), src_pages, dst_pool,
-                                            long(dst_page_bytes / 16), dst_pages, n_vec);
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 

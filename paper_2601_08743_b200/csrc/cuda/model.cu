@@ -325,8 +325,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
                 e1 = timing_event();
                 TKV_CUDA_CHECK(cudaEventRecord(e0, s));
             }
-            static const bool old_gather = std::getenv("TKV_GATHER_OLD") != nullptr;  // A/B switch
-            if (a.gather_chunks && a.gather_in == DType::bf16 && !old_gather && !(a.gather_page_bytes & (a.gather_page_bytes - 1)))
+            if (a.gather_chunks && a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1)))
                 launch_gather_rope_bf16(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_chunks,
                                         a.gather_n_chunks, c.num_layers, l, kvd, c.head_dim, rope_.cos_f(), rope_.sin_f(),
                                         const_cast<void*>(a.ctx_k), const_cast<void*>(a.ctx_v), a.ctx_rows, s);
