@@ -178,7 +178,8 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=12288, help="2 MiB HBM pages in the fast-tier pool")
     ap.add_argument("--b_c", type=int, default=100)
     ap.add_argument("--b_m", type=int, default=10)
-    ap.add_argument("--copy-engine", type=int, default=0)
+    ap.add_argument("--copy-engine", type=int, default=0, help="0: DMA copy engines, 1: SM 16-byte copy kernel")
+    ap.add_argument("--sm-copy-ctas", type=int, default=16)
     ap.add_argument("--nocache-queries", type=int, default=300, help="queries in the no-cache comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--peer-fetch", type=int, default=None,
@@ -245,7 +246,7 @@ def main():
             peer_status = peer_status if peer_status != "on" else "off (a peer failed to attach)"
 
     opts = N.serve_options(rerank_on=0, pipeline_on=1, capacity=args.capacity, policy=args.policy, b_c=args.b_c,
-                           b_m=args.b_m, copy_engine=args.copy_engine, time_kernels=1,
+                           b_m=args.b_m, copy_engine=args.copy_engine, sm_copy_ctas=args.sm_copy_ctas, time_kernels=1,
                            peer_fetch=int(peer_status == "on"))
 
     rerank_ms = []
