@@ -384,7 +384,11 @@ def main():
                      "traffic_source": traffic.get("source"), "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "share_of_step": gemm_ms / dev_ms if dev_ms else None},
-        "gather": {"ms_per_step": sum(r["gather_ms"] for r in results) / args.steps},
+        "gather": {"ms_per_step": sum(r["gather_ms"] for r in results) / args.steps,
+                   "gbs": (sum(r["gather_bytes"] for r in results) / (sum(r["gather_ms"] for r in results) / 1e3) / 1e9
+                           if sum(r["gather_ms"] for r in results) else None),
+                   "peak_gbs": peaks.get("hbm_gbs"),
+                   "bytes_definition": "prefix rows x 2 (K,V) x layers x kv_dim x (read + write element bytes)"},
         "global_rerank_ms_per_step": sum(timed_rerank_ms) / args.steps,
         "attention_ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
         "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,

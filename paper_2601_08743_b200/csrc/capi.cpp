@@ -192,6 +192,7 @@ json serve_result_json(const tkv::ServeResult& R) {
             {"gemm_ms", R.gemm_ms},
             {"gemm_flops", R.gemm_flops},
             {"gather_ms", R.gather_ms},
+            {"gather_bytes", R.gather_bytes},
             {"attn_ms", R.attn_ms},
             {"ctx_tokens", R.total_ctx_tokens},
             {"suffix_tokens", R.total_suffix_tokens}};
