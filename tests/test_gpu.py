@@ -397,3 +397,46 @@ def test_executor_replays_c2_reference_traces(run_name):
     assert s.info()["free_pages"] == 4096
     s.close()
     m.close()
+
+
+def test_executor_edge_cases():
+    """Ragged and degenerate batches through the bf16 executor: a query matching no table, an
+    empty suffix (no prefill, no first token: argmax stays -1), suffixes of 1..300 tokens, a table
+    image spanning many pages, a one-query batch; each first token equals the query run alone.
+    Unknown tables and an undersized pool fail loudly with the reference error / a clear message."""
+    kw = dict(num_layers=2, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=330, ffn_dim=512, mlp="swiglu",
+              norm="rms")
+    m = N.Model(dtype="bf16", **kw)
+    s = N.Store(m, page_bytes=16 << 10, n_pages=4096)  # 16 KiB pages: every table spans 3-12 pages
+    eng = N.Engine(demo_path("demo_schema.json"))
+    s.precompute(eng)
+    rng = np.random.default_rng(11)
+    base = _demo_queries(8)
+    qs = [([], rng.integers(0, 330, 9).tolist()),           # no table
+          (base[0][0], []),                                 # empty suffix
+          (base[1][0], [int(rng.integers(0, 330))]),        # one token
+          (base[2][0], rng.integers(0, 330, 300).tolist()),  # long suffix
+          (base[3][0], base[3][1])]
+    res = s.serve(qs, capacity=6, b_c=2, b_m=1, want_logits=True)
+    assert sorted(res["order"]) == list(range(len(qs)))
+    for i, qi in enumerate(res["order"]):
+        tables, suffix = qs[qi]
+        if not suffix:
+            assert res["argmax"][i] == -1
+            continue
+        k, v = s.assemble(tables) if tables else (None, None)
+        ref = m.forward(suffix, mode=0, ctx_k=k, ctx_v=v)
+        assert np.abs(res["logits"][i] - ref["logits"]).max() <= 3e-2, qi
+    one = s.serve([qs[4]], capacity=6, b_c=100, b_m=10, want_logits=True)
+    assert one["order"] == [0] and len(one["ttft_ms"]) == 1
+    with pytest.raises(N.TkvError) as e:
+        s.serve([([99], [1, 2, 3])], capacity=6)
+    assert e.value.name == "UnknownTable"
+    tiny = N.Store(m, page_bytes=16 << 10, n_pages=4)
+    tiny.precompute(eng)
+    with pytest.raises(N.TkvError) as e:
+        tiny.serve(base[:2], capacity=6)
+    assert "page pool" in e.value.msg or "pool" in e.value.msg
+    tiny.close()
+    s.close()
+    m.close()
