@@ -26,19 +26,25 @@ StagingRing::~StagingRing() {
     cudaFree(dev_);
 }
 
-void* StagingRing::upload(const void* src, size_t n, cudaStream_t s) {
-    n = (n + 255) & ~size_t(255);
+void* StagingRing::upload(const void* src, size_t bytes, cudaStream_t s) {
+    const size_t n = (bytes + 255) & ~size_t(255);  // keep every chunk 256-byte aligned
+    reserve(n);
+    if (bytes) {
+        std::memcpy(host_ + off_, src, bytes);
+        TKV_CUDA_CHECK(cudaMemcpyAsync(dev_ + off_, host_ + off_, bytes, cudaMemcpyHostToDevice, s));
+    }
+    void* d = dev_ + off_;
+    off_ += n;
+    return d;
+}
+
+void StagingRing::reserve(size_t n) {
     if (n > cap_) throw std::runtime_error("staging ring too small for one upload");
     if (off_ + n > cap_) {
         // wrap: every earlier chunk may still be read by queued work
         TKV_CUDA_CHECK(cudaDeviceSynchronize());
         off_ = 0;
     }
-    std::memcpy(host_ + off_, src, n);
-    TKV_CUDA_CHECK(cudaMemcpyAsync(dev_ + off_, host_ + off_, n, cudaMemcpyHostToDevice, s));
-    void* d = dev_ + off_;
-    off_ += n;
-    return d;
 }
 
 // ------------------------------------------------------------------ RopeTables

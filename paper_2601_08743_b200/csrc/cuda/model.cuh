@@ -35,6 +35,8 @@ class StagingRing {
     ~StagingRing();
     // copies `n` bytes of `src` into the ring and enqueues the H2D copy on `s`; returns the device pointer
     void* upload(const void* src, size_t n, cudaStream_t s);
+    // make room for n more bytes without wrapping (wraps, with a device sync, now if needed)
+    void reserve(size_t n);
 
    private:
     uint8_t* host_ = nullptr;
