@@ -315,16 +315,19 @@ def main():
     cached_sub = store.serve(qs_nc, N.serve_options(rerank_on=0, capacity=args.capacity, policy=args.policy, b_c=args.b_c,
                                                     b_m=args.b_m))
     # ---- e2e: prompt text in, first tokens out, through the C ABI (wall clock)
-    e2e_texts = [entries[i][1] for i in my_slice(global_order())]
+    # the user path: the rank's prompts in arrival order; serve_text reranks them itself
+    e2e_texts = [entries[i][1] for i in sorted(my_slice(global_order()))]
     e2e_opts = N.serve_options(rerank_on=1, capacity=args.capacity, policy=args.policy, b_c=args.b_c, b_m=args.b_m)
     for _ in range(args.warmup):
         store.serve_text(eng, e2e_texts, options=e2e_opts)
     barrier()
     te = time.perf_counter()
+    e2e_steps = []
     for _ in range(args.steps):  # prompt text in (host analysis, H2D), first tokens out (D2H), per step
         tc = time.perf_counter()
         e2e_res = store.serve_text(eng, e2e_texts, options=e2e_opts)
         e2e_last_wall = time.perf_counter() - tc
+        e2e_steps.append([round(e2e_last_wall * 1e3, 1), round(e2e_res["makespan_ms"], 1), round(e2e_res["wall_ms"], 1)])
     e2e_s = (time.perf_counter() - te) / args.steps
     if world > 1:
         t = torch.tensor([e2e_s], device=coll_dev)
@@ -395,7 +398,8 @@ def main():
                 "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5),
                 "last_step_ms": {"prompt_analysis": e2e_res.get("analyze_ms"), "host_enqueue": e2e_res["host_ms"],
                                  "device_makespan": e2e_res["makespan_ms"], "serve_wall": e2e_res["wall_ms"],
-                                 "call_wall": e2e_last_wall * 1e3}},
+                                 "call_wall": e2e_last_wall * 1e3},
+                "steps_call_makespan_serve_ms": e2e_steps},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

@@ -145,6 +145,8 @@ void Server::set_peer_plan(int slot, PeerPlan plan) {
 Server::~Server() {
     cudaDeviceSynchronize();
     cudaFree(ctx_buf_);
+    cudaFree(argmax_buf_);
+    cudaFree(logits_buf_);
     cudaStreamDestroy(cs_);
     cudaStreamDestroy(ds_);
     cudaStreamDestroy(ps_);
@@ -154,6 +156,23 @@ Server::~Server() {
 void Server::set_table_tokens(std::vector<std::vector<int32_t>> tt, std::vector<int> group_of) {
     table_tokens_ = std::move(tt);
     group_of_ = std::move(group_of);
+}
+
+void Server::ensure_out(size_t n_argmax, size_t n_logits) {
+    // per-batch outputs stay allocated across calls: no allocator traffic (and no implicit
+    // synchronisation or pool trimming) inside a serve
+    if (n_argmax > argmax_cap_) {
+        TKV_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(argmax_buf_);
+        argmax_cap_ = std::max(n_argmax, argmax_cap_ * 2);
+        TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&argmax_buf_), argmax_cap_ * sizeof(int32_t)));
+    }
+    if (n_logits > logits_cap_) {
+        TKV_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(logits_buf_);
+        logits_cap_ = std::max(n_logits, logits_cap_ * 2);
+        TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&logits_buf_), logits_cap_ * sizeof(float)));
+    }
 }
 
 void Server::ensure_ctx(size_t bytes) {
@@ -249,8 +268,9 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     const int vp = mc.vocab_padded();
     size_t max_q = 0;
     for (const auto& w : plan.windows) max_q = std::max(max_q, w.end - w.begin);
-    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_argmax), sizeof(int32_t) * queries.size(), cs_));
-    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_logits), sizeof(float) * max_q * vp, cs_));
+    ensure_out(queries.size(), max_q * size_t(vp));
+    d_argmax = argmax_buf_;
+    d_logits = logits_buf_;
     std::vector<float> logits_host;
     if (opts.keep_logits) logits_host.resize(queries.size() * size_t(vp));
 
@@ -558,10 +578,12 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     if (host_prof)
         std::fprintf(stderr, "[tkv host] plan %.1f ms, copies %.1f ms, forward enqueue %.1f ms, rest %.1f ms (windows %zu)\n",
                      hp_plan, hp_copy, hp_fwd, hp_rest, plan.windows.size());
+    const double tail0 = now_ms();
     TKV_CUDA_CHECK(cudaStreamSynchronize(ps_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(ds_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(xs_));
     TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+    const double tail1 = now_ms();
     if (peering) {
         unsigned long long st[2];
         TKV_CUDA_CHECK(cudaMemcpy(st, mesh_->stats(), sizeof(st), cudaMemcpyDeviceToHost));
@@ -584,9 +606,10 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     }
     if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
     if (opts.keep_logits) R.logits = std::move(logits_host);
-    TKV_CUDA_CHECK(cudaFree(d_argmax));
-    TKV_CUDA_CHECK(cudaFree(d_logits));
     R.wall_ms = now_ms() - host0;
+    if (host_prof)
+        std::fprintf(stderr, "[tkv host] tail: sync %.1f ms, results %.1f ms; makespan %.1f, wall %.1f\n", tail1 - tail0,
+                     now_ms() - tail1, R.makespan_ms, R.wall_ms);
     return R;
 }
 
@@ -620,8 +643,9 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
     model_.rope().ensure(max_pos);
     int32_t* d_argmax = nullptr;
     float* d_logits = nullptr;
-    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_argmax), sizeof(int32_t) * n, cs_));
-    TKV_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d_logits), sizeof(float) * bc * vp, cs_));
+    ensure_out(n, bc * size_t(vp));
+    d_argmax = argmax_buf_;
+    d_logits = logits_buf_;
     std::vector<float> logits_host;
     if (opts.keep_logits) logits_host.resize(n * size_t(vp));
     R.window_of.assign(n, 0);
@@ -723,8 +747,6 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
     R.makespan_ms = R.window_end_ms.back();
     if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
     if (opts.keep_logits) R.logits = std::move(logits_host);
-    TKV_CUDA_CHECK(cudaFree(d_argmax));
-    TKV_CUDA_CHECK(cudaFree(d_logits));
     return R;
 }
 

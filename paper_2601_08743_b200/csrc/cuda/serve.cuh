@@ -107,6 +107,7 @@ class Server {
 
    private:
     void ensure_ctx(size_t bytes);
+    void ensure_out(size_t n_argmax, size_t n_logits);
     Model& model_;
     Arena& arena_;
     PagePool& pool_;
@@ -116,6 +117,9 @@ class Server {
     std::unordered_map<int, PeerPlan> peer_plans_;
     void* ctx_buf_ = nullptr;
     size_t ctx_cap_ = 0;
+    int32_t* argmax_buf_ = nullptr;
+    float* logits_buf_ = nullptr;
+    size_t argmax_cap_ = 0, logits_cap_ = 0;
     std::vector<std::vector<int32_t>> table_tokens_;
     std::vector<int> group_of_;
 };
