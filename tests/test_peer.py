@@ -61,6 +61,23 @@ def _worker(rank, world, port, out_dir):
         out["revoked"] = [got.tobytes() == payload[0], from_peer]
     dist.barrier()
 
+    # ---- race: rank 1 publishes and revokes tables in a loop while rank 0 fetches them; every
+    # fetch must land the exact payload whichever source each CTA ended up reading
+    if rank == 1:
+        for it in range(120):
+            t = it % 12
+            s.peer_publish(t)
+            s.peer_unpublish(t)
+    else:
+        ok, from_peer = True, 0
+        for it in range(240):
+            t = (it * 7) % 12
+            got, fp = s.peer_fetch(t, len(payload[t]))
+            ok &= got.tobytes() == payload[t]
+            from_peer += fp
+        out["race"] = [ok, from_peer]
+    dist.barrier()
+
     # ---- serving: each rank serves its half of the demo chain with the other's plan
     g = load("demo64")["result"]
     qs = [(q["assembly_order"], q["remainder"]) for q in g["queries"][:64]]
@@ -112,6 +129,7 @@ def test_peer_fetch_bytes_and_sources(two_ranks):
         assert from_peer == (n if t < 6 else 0), (t, from_peer, n)
     exact, from_peer = r0["revoked"]
     assert exact and from_peer == 0  # a revoked entry is never read
+    assert r0["race"][0]  # bytes exact under concurrent publish/revoke
 
 
 def test_peer_fetch_leaves_trace_and_first_tokens_unchanged(two_ranks):
