@@ -90,6 +90,8 @@ class ClockSampler:
 
 def build_workload(cfg_name, n_queries_total):
     from paper_2601_08743_b200 import workloads as W
+    if cfg_name == "c1":  # the reference default: the 12-table demo schema, gen_demo queries
+        return W.demo_schema(), W.demo_workload(n_queries_total)
     spec = W.CONFIGS[cfg_name]
     spec = W.SpiderSpec(**{**spec.__dict__, "n_queries": n_queries_total})
     tables, entries, _ = W.spider_like(spec)
@@ -140,6 +142,25 @@ def reference_arm(args, rank, world):
     print(json.dumps(line))
 
 
+def cpu_baseline_demo(tables, entries, threads):
+    """C1: the reference's own demo path (assemble + query_attend per query, the unchanged library)
+    on `threads` host cores — measured in full, nothing extrapolated."""
+    import tempfile
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    from paper_2601_08743_b200 import workloads as W
+    with tempfile.TemporaryDirectory() as d:
+        sp, wp = W.write_corpus(d, tables, entries)
+        out = subprocess.run([exe, "demo", sp, wp, str(len(entries)), str(threads)], capture_output=True, text=True,
+                             check=True)
+    r = json.loads(out.stdout)
+    return {"value": r["cached_qps"], "unit": "queries/s", "cores": threads, "kind": "reference",
+            "sample": "all %d demo queries, reference assemble + query_attend (f32, double accumulate), %d threads; "
+                      "no-cache prefill %.1f queries/s" % (len(entries), threads, r["nocache_qps"]),
+            "p50_query_ms": r["cached_p50_ms"], "p99_query_ms": r["cached_p99_ms"]}
+
+
 def cpu_baseline_sample(eng, entries, n=4):
     """Bounded CPU baseline on this host (rank 0, N=1): the unchanged reference library timing one
     layer of query_attend at hidden 4096 for n queries in parallel, extrapolated to 32 layers."""
@@ -170,14 +191,15 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"],
+                    help="c1 = BASELINE configs[0]: reference default (tiny model, f32 reference arithmetic, demo)")
     ap.add_argument("--queries", type=int, default=1000, help="queries per GPU")
     ap.add_argument("--layers", type=int, default=LLAMA8B["num_layers"])
-    ap.add_argument("--capacity", type=int, default=32)
+    ap.add_argument("--capacity", type=int, default=None, help="cache entries (default 32; c1: 6)")
     ap.add_argument("--policy", default="lru", choices=["lru", "fifo", "lfu"])
     ap.add_argument("--pool-pages", type=int, default=12288, help="2 MiB HBM pages in the fast-tier pool")
-    ap.add_argument("--b_c", type=int, default=100)
-    ap.add_argument("--b_m", type=int, default=10)
+    ap.add_argument("--b_c", type=int, default=None, help="default 100 (c1: 1)")
+    ap.add_argument("--b_m", type=int, default=None, help="default 10 (c1: 1)")
     ap.add_argument("--copy-engine", type=int, default=0, help="0: DMA copy engines, 1: SM 16-byte copy kernel")
     ap.add_argument("--sm-copy-ctas", type=int, default=16)
     ap.add_argument("--nocache-queries", type=int, default=300, help="queries in the no-cache comparison")
@@ -186,6 +208,16 @@ def main():
                     help="NVLink peer KV fetch between ranks (default: on when N > 1)")
     args = ap.parse_args()
 
+    c1 = args.config == "c1"
+    if args.capacity is None:
+        args.capacity = 6 if c1 else 32
+    if args.b_c is None:
+        args.b_c = 1 if c1 else 100
+    if args.b_m is None:
+        args.b_m = 1 if c1 else 10
+    if c1:
+        args.queries = min(args.queries, 64) if args.queries != 1000 else 64
+        args.nocache_queries = min(args.nocache_queries, args.queries)
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, rank, world)
@@ -211,8 +243,13 @@ def main():
     eng = N.Engine(corpus_json=W.dump_schema_corpus(tables))
     mk = dict(LLAMA8B, num_layers=args.layers)
     t0 = time.time()
-    model = N.Model(dtype="bf16", device=local, **mk)
-    store = N.Store(model, page_bytes=2 << 20, n_pages=args.pool_pages)
+    if c1:  # the reference's own model (model.hpp defaults) in f32 with the reference arithmetic
+        model = N.Model(dtype="f32", device=local, num_layers=2, num_heads=4, head_dim=16,
+                        vocab_size=eng.info["vocab_size"])
+        store = N.Store(model, page_bytes=64 << 10, n_pages=2048)
+    else:
+        model = N.Model(dtype="bf16", device=local, **mk)
+        store = N.Store(model, page_bytes=2 << 20, n_pages=args.pool_pages)
     store.precompute(eng)
     store.bind_engine(eng)
     setup_s = time.time() - t0
@@ -349,7 +386,9 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_sample(eng, entries, n=8)
+            import multiprocessing
+            cpu = (cpu_baseline_demo(tables, entries, min(8, multiprocessing.cpu_count())) if c1
+                   else cpu_baseline_sample(eng, entries, n=8))
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unavailable": str(e)}
     nc_p50, c_p50 = pct(nc["ttft_ms"], 0.5), pct(cached_sub["ttft_ms"], 0.5)
@@ -357,13 +396,18 @@ def main():
         "metric": "prefill queries/sec (cached path); p50/p99 TTFT vs no-cache prefill; KV load GB/s vs PCIe",
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "%s Spider-like: %d DBs / %d tables, Zipf(1.1), %d queries per GPU; Llama-3-8B-shaped "
-                               "(%d layers, 32q/8kv x128, SwiGLU 14336, RMSNorm, vocab 128256), random weights"
-                               % (args.config, W.CONFIGS[args.config].n_db, len(tables), n_local, args.layers),
-                   "cache": "%s C=%d tables, b_c=%d, b_m=%d, rerank on, 2 MiB HBM pages" % (args.policy.upper(), args.capacity, args.b_c, args.b_m),
+        "vs_baseline": None, "dtype": "f32" if c1 else "bf16", "data": "synthetic",
+        "config": {"workload": ("c1 reference default: 12-table demo schema, %d gen_demo queries, the reference model "
+                                "(2 layers, 4 heads x 16, LayerNorm, SiLU FFN) in f32 with the reference arithmetic"
+                                % n_local) if c1 else
+                               ("%s Spider-like: %d DBs / %d tables, Zipf(1.1), %d queries per GPU; Llama-3-8B-shaped "
+                                "(%d layers, 32q/8kv x128, SwiGLU 14336, RMSNorm, vocab 128256), random weights"
+                                % (args.config, W.CONFIGS[args.config].n_db, len(tables), n_local, args.layers)),
+                   "cache": "%s C=%d tables, b_c=%d, b_m=%d, rerank on, %s HBM pages"
+                            % (args.policy.upper(), args.capacity, args.b_c, args.b_m, "64 KiB" if c1 else "2 MiB"),
                    "parallelism": "dp%d (request slices of the global rerank)" % world,
-                   "l2": "inputs larger than L2 (16 GB weights streamed per window)"},
+                   "l2": "small model: weights and KV stay L2-resident (a latency-bound parity config)" if c1 else
+                         "inputs larger than L2 (16 GB weights streamed per window)"},
         "p50_ttft_ms": pct(ttfts, 0.5), "p99_ttft_ms": pct(ttfts, 0.99),
         "nocache": {"queries": nc_n, "p50_ttft_ms": nc_p50, "p99_ttft_ms": pct(nc["ttft_ms"], 0.99),
                     "qps": nc_n / (nc["makespan_ms"] / 1e3), "cached_p50_ttft_ms_same_subset": c_p50,
@@ -381,7 +425,11 @@ def main():
                     "peer_bytes_per_step": sum(r["peer_bytes"] for r in results) / args.steps,
                     "peer_fallback_bytes_per_step": sum(r["peer_fallback_bytes"] for r in results) / args.steps,
                     "hits_misses_swaps_prefetch": results[0]["counters"]},
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
+        "roofline": {"bound": "latency", "kernel": "reference-precision SIMT forward (simt.cu)", "achieved": None,
+                     "peak": None, "unit": None, "frac": None, "traffic": None,
+                     "note": "c1 runs the reference's f32/double arithmetic for bit-level parity; tensor-core "
+                             "rooflines are reported on c2-c5"} if c1 else
+                    {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": traffic.get("dram_bytes_per_launch"),
                      "traffic_source": traffic.get("source"), "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
