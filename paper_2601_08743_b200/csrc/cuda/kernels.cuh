@@ -79,6 +79,7 @@ struct AttnSeq {
 };
 void launch_attend_ref(const void* q, const void* k_own, const void* v_own, const void* k_ctx, const void* v_ctx,
                        const int32_t* group, const AttnSeq* seqs, int n_seqs, int total_q, void* out, DType dt,
-                       int num_heads, int kv_heads, int head_dim, int mode, cudaStream_t s);
+                       int num_heads, int kv_heads, int head_dim, int mode, cudaStream_t s,
+                       const AttnSeq* seqs_host = nullptr);
 
 }  // namespace tkv

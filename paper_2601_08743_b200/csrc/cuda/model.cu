@@ -468,7 +468,7 @@ void Model::forward_ref(const FwdArgs& a, cudaStream_t s) {
         const void* kc = a.ctx_k ? static_cast<const uint8_t*>(a.ctx_k) + ctx_off : k;
         const void* vc = a.ctx_v ? static_cast<const uint8_t*>(a.ctx_v) + ctx_off : v_l;
         launch_attend_ref(q, k, v_l, kc, vc, a.group, a.seqs, a.n_seqs, M, att, dt, c.num_heads, c.kv_heads, c.head_dim,
-                          a.mode, s);
+                          a.mode, s, a.seqs_host);
         launch_matmul_ref(L.wo, att, proj, dt, h, qd, M, 0, s);
         launch_add_ref(x, proj, dt, long(M) * h, s);
         launch_layer_norm_ref(x, xn, dt, M, h, rms, c.eps, s);

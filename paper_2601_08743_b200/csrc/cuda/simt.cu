@@ -8,6 +8,8 @@
 // wrappers); the bf16 tensor-core path (gemm_tc.cu, attn_tc.cu) is the performance path.
 #include <algorithm>
 
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -232,17 +234,18 @@ void launch_rope_ref(void* x, DType dt, const int64_t* positions, int n, int hea
 
 void launch_attend_ref(const void* q, const void* k_own, const void* v_own, const void* k_ctx, const void* v_ctx,
                        const int32_t* group, const AttnSeq* seqs, int n_seqs, int total_q, void* out, DType dt,
-                       int num_heads, int kv_heads, int head_dim, int mode, cudaStream_t s) {
+                       int num_heads, int kv_heads, int head_dim, int mode, cudaStream_t s, const AttnSeq* seqs_host) {
     if (total_q == 0) return;
-    // scratch for one score row per (row, head): bounded by the longest combined key range
+    // scratch for one score row per (row, head): bounded by the longest combined key range, taken
+    // from the host copy of the sequence table (read back from the device only without one)
     int max_keys = 0;
-    {
-        // seqs live on the device; the caller guarantees max_keys via a host-side copy below
-        AttnSeq* hs = new AttnSeq[n_seqs];
-        TKV_CUDA_CHECK(cudaMemcpyAsync(hs, seqs, sizeof(AttnSeq) * n_seqs, cudaMemcpyDeviceToHost, s));
+    if (seqs_host) {
+        for (int i = 0; i < n_seqs; ++i) max_keys = std::max(max_keys, seqs_host[i].n_ctx + seqs_host[i].n_own);
+    } else {
+        std::vector<AttnSeq> hs(static_cast<size_t>(n_seqs));
+        TKV_CUDA_CHECK(cudaMemcpyAsync(hs.data(), seqs, sizeof(AttnSeq) * n_seqs, cudaMemcpyDeviceToHost, s));
         TKV_CUDA_CHECK(cudaStreamSynchronize(s));
-        for (int i = 0; i < n_seqs; ++i) max_keys = std::max(max_keys, hs[i].n_ctx + hs[i].n_own);
-        delete[] hs;
+        for (const auto& h : hs) max_keys = std::max(max_keys, h.n_ctx + h.n_own);
     }
     double* scratch = nullptr;
     const size_t bytes = size_t(total_q) * num_heads * std::max(1, max_keys) * sizeof(double);
