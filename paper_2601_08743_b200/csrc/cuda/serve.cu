@@ -242,18 +242,46 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         return o;
     };
 
-    // ---- sizing: context slab for the largest window, rope table for the longest row
+    // ---- compute groups: consecutive windows with tiny suffixes (the reference's b_c = 1 demo
+    // configuration) share one prefill; a group closes once it holds kGroupRows suffix rows, which a
+    // single window of the serving configurations already does (so those run one window at a time).
+    // Copies, the cache trace and page lifetimes stay per window; a query's TTFT is its group's end.
+    constexpr long kGroupRows = 1024;
+    constexpr int kGroupWindows = 64;
+    const bool grouping = mesh_ == nullptr && !peering;
+    std::vector<char> closes(plan.windows.size(), 1);
+    if (grouping) {
+        long rows = 0;
+        int nw = 0;
+        for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
+            for (size_t qi = plan.windows[wi].begin; qi < plan.windows[wi].end; ++qi) rows += long(queries[R.order[qi]].suffix.size());
+            ++nw;
+            closes[wi] = rows >= kGroupRows || nw >= kGroupWindows || wi + 1 == plan.windows.size();
+            if (closes[wi]) rows = 0, nw = 0;
+        }
+    }
+    // ---- sizing: context slab for the largest group, rope table for the longest row
     long max_ctx_rows = 0;
     int max_pos = 1;
-    for (const auto& w : plan.windows) {
+    size_t max_q = 0;
+    {
         long rows = 0;
-        for (size_t qi = w.begin; qi < w.end; ++qi) {
-            long c = 0;
-            for (int t : plan.queries[qi].tables) c += arena_.find(t)->tokens;
-            rows += c;
-            max_pos = std::max<int>(max_pos, int(c + long(queries[R.order[qi]].suffix.size()) + 1));
+        size_t nq = 0;
+        for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
+            const auto& w = plan.windows[wi];
+            for (size_t qi = w.begin; qi < w.end; ++qi) {
+                long c = 0;
+                for (int t : plan.queries[qi].tables) c += arena_.find(t)->tokens;
+                rows += c;
+                max_pos = std::max<int>(max_pos, int(c + long(queries[R.order[qi]].suffix.size()) + 1));
+            }
+            nq += w.end - w.begin;
+            if (closes[wi]) {
+                max_ctx_rows = std::max(max_ctx_rows, rows);
+                max_q = std::max(max_q, nq);
+                rows = 0, nq = 0;
+            }
         }
-        max_ctx_rows = std::max(max_ctx_rows, rows);
     }
     model_.rope().ensure(max_pos);
     // bf16 serving streams the prefix one layer at a time (gathered right before that layer's
@@ -266,8 +294,6 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     int32_t* d_argmax = nullptr;
     float* d_logits = nullptr;
     const int vp = mc.vocab_padded();
-    size_t max_q = 0;
-    for (const auto& w : plan.windows) max_q = std::max(max_q, w.end - w.begin);
     ensure_out(queries.size(), max_q * size_t(vp));
     d_argmax = argmax_buf_;
     d_logits = logits_buf_;
@@ -337,11 +363,22 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     R.window_of.assign(plan.queries.size(), 0);
     R.argmax.assign(plan.queries.size(), -1);
 
+    // the open compute group's accumulated prefill inputs
+    std::vector<GatherSeg> segs;
+    std::vector<int32_t> page_ids, tokens, pos, logit_rows;
+    std::vector<int64_t> pos64;
+    std::vector<AttnSeq> seqs;
+    std::vector<size_t> seq_query;
+    int ctx_rows = 0, M = 0;
+    size_t group_first = 0;  // first window of the open group
+    bool in_dt_set = false;
+    DType in_dt_s = DType::bf16;
+    std::vector<std::pair<int, std::vector<int32_t>>> dropped;  // evicted in the group: recycle after its compute
+
     hp_tick(hp_plan);
     for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
         const auto& w = plan.windows[wi];
         const auto& wt = tr.windows[wi];
-        std::vector<std::pair<int, std::vector<int32_t>>> dropped;  // evicted this window: recycle after compute(wi)
         cur_window = wi;
         pub_now.swap(pub_next);  // prefetches of the previous window
         pub_next.clear();
@@ -437,12 +474,6 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         }
         pub_now.clear();
 
-        std::vector<GatherSeg> segs;
-        std::vector<int32_t> page_ids, tokens, pos, logit_rows;
-        std::vector<int64_t> pos64;
-        std::vector<AttnSeq> seqs;
-        std::vector<size_t> seq_query;
-        int ctx_rows = 0, M = 0;
         for (size_t qi = w.begin; qi < w.end; ++qi) {
             const ServeQuery& q = queries[R.order[qi]];
             R.window_of[qi] = int(wi);
@@ -466,13 +497,18 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             M += int(q.suffix.size());
             logit_rows.push_back(M - 1);
         }
+        for (const auto& qs : qsegs)
+            if (!qs.empty() && !in_dt_set) {  // the arena holds one dtype per corpus
+                in_dt_s = arena_.find(qs.front().table)->dtype;
+                in_dt_set = true;
+            }
+        if (!closes[wi]) continue;  // the group stays open: this window computes with the next ones
         R.total_suffix_tokens += M;
         StagingRing& ring = model_.ring();
         const GatherSeg* d_segs_s = nullptr;
         const int32_t* d_pages_s = nullptr;
         const int4* d_chunks_s = nullptr;
         int n_chunks_s = 0;
-        DType in_dt_s = DType::bf16;
         if (ctx_rows > 0 && stream_ctx && M > 0) {
             d_segs_s = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
             d_pages_s = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
@@ -481,22 +517,12 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             d_chunks_s = static_cast<const int4*>(ring.upload(chunks.data(), chunks.size() * sizeof(int4), cs_));
             R.meta_bytes += chunks.size() * sizeof(int4);
             R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
-            for (const auto& qs : qsegs)
-                if (!qs.empty()) {
-                    in_dt_s = arena_.find(qs.front().table)->dtype;
-                    break;
-                }
             if (opts.time_kernels) R.gather_bytes += double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt_s) + oes);
         } else if (ctx_rows > 0 && !stream_ctx) {
             auto* d_segs = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
             auto* d_pages = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
             R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
-            DType in_dt = DType::f32;  // the arena holds one dtype per corpus (f32 .kv files or bf16 encodes)
-            for (const auto& qs : qsegs)
-                if (!qs.empty()) {
-                    in_dt = arena_.find(qs.front().table)->dtype;
-                    break;
-                }
+            const DType in_dt = in_dt_set ? in_dt_s : DType::f32;
             cudaEvent_t g0 = nullptr, g1 = nullptr;
             if (opts.time_kernels) {
                 g0 = evp.get();
@@ -541,7 +567,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             fa.logit_rows_host = logit_rows.data();
             fa.n_logit_rows = int(logit_rows.size());
             fa.logits_out = d_logits;
-            fa.argmax_out = d_argmax + w.begin;  // compacted per window; remapped below
+            fa.argmax_out = d_argmax + plan.windows[group_first].begin;  // compacted per group; remapped below
             R.meta_bytes += tokens.size() * 16 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
             hp_tick(hp_rest);
             model_.set_timing(opts.time_kernels);
@@ -555,8 +581,9 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
             }
         }
-        win_end[wi] = evp.get();
-        TKV_CUDA_CHECK(cudaEventRecord(win_end[wi], cs_));
+        cudaEvent_t ge = evp.get();
+        TKV_CUDA_CHECK(cudaEventRecord(ge, cs_));
+        for (size_t gw = group_first; gw <= wi; ++gw) win_end[gw] = ge;
         for (auto& [t, pg] : dropped) {
             auto it = t >= 0 ? published.find(t) : published.end();
             if (it != published.end() && it->second == pg) {  // peers must drain before the pages recycle
@@ -565,8 +592,14 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             }
             pool_.release(pg, cs_);
         }
-        // the k-th prefilling query of this window writes its argmax to d_argmax[w.begin + k]
-        for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(w.begin + k);  // slot, resolved below
+        // the k-th prefilling query of this group writes its argmax to d_argmax[first begin + k]
+        for (size_t k = 0; k < seq_query.size(); ++k)
+            R.argmax[seq_query[k]] = int32_t(plan.windows[group_first].begin + k);  // slot, resolved below
+        dropped.clear();
+        segs.clear(), page_ids.clear(), tokens.clear(), pos.clear(), logit_rows.clear(), pos64.clear();
+        seqs.clear(), seq_query.clear();
+        ctx_rows = 0, M = 0;
+        group_first = wi + 1;
     }
     // the batch's cache dies with it: every still-resident table's pages go back to the pool
     for (auto& kv : published) launch_dir_revoke(mesh_->local_dir(), kv.first, cs_);
@@ -641,98 +674,109 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
         max_pos = std::max<int>(max_pos, int(c));
     }
     model_.rope().ensure(max_pos);
+    // Sub-batches in served order: at most kMaxRows prompt rows each (bounded activation workspace),
+    // and consecutive tiny windows share one (the same kGroupRows grouping as the cached path); a
+    // query's first token is ready when its sub-batch ends.
+    constexpr long kMaxRows = 65536, kGroupRows = 1024;
+    auto prompt_rows = [&](size_t qi) {
+        const ServeQuery& q = queries[R.order[qi]];
+        long len = long(q.suffix.size());
+        for (int t : q.tables) len += long(table_tokens_[size_t(t)].size());
+        return len;
+    };
+    std::vector<std::pair<size_t, size_t>> subs;  // [first, last) served indices
+    {
+        size_t a = 0;
+        long rows = 0;
+        for (size_t qi = 0; qi < n; ++qi) {
+            const long len = prompt_rows(qi);
+            if (qi > a && rows + len > kMaxRows) subs.push_back({a, qi}), a = qi, rows = 0;
+            rows += len;
+            const bool window_end = (qi + 1) % bc == 0 || qi + 1 == n;
+            if (qi + 1 == n || (window_end && rows >= kGroupRows)) subs.push_back({a, qi + 1}), a = qi + 1, rows = 0;
+        }
+    }
+    size_t max_sub = 1;
+    for (const auto& sb : subs) max_sub = std::max(max_sub, sb.second - sb.first);
     int32_t* d_argmax = nullptr;
     float* d_logits = nullptr;
-    ensure_out(n, bc * size_t(vp));
+    ensure_out(n, max_sub * size_t(vp));
     d_argmax = argmax_buf_;
     d_logits = logits_buf_;
     std::vector<float> logits_host;
     if (opts.keep_logits) logits_host.resize(n * size_t(vp));
     R.window_of.assign(n, 0);
     R.argmax.assign(n, -1);
-    std::vector<cudaEvent_t> win_end;
-    // Each window is prefilled in sub-batches of at most kMaxRows prompt rows (bounded activation
-    // workspace); a query's first token is ready when its sub-batch ends.
-    constexpr long kMaxRows = 65536;
+    std::vector<cudaEvent_t> win_end((n + bc - 1) / bc, nullptr);
     std::vector<cudaEvent_t> sub_end;
     std::vector<int> sub_of(n, -1);
-    for (size_t b = 0, wi = 0; b < n; b += bc, ++wi) {
-        const size_t e = std::min(n, b + bc);
-        size_t slot = b;  // argmax slots of this window's prefilling queries: b, b + 1, ...
-        for (size_t qb = b; qb < e;) {
-            std::vector<int32_t> tokens, pos, group, logit_rows;
-            std::vector<int64_t> pos64;
-            std::vector<AttnSeq> seqs;
-            std::vector<size_t> seq_query;
-            int M = 0;
-            size_t qi = qb;
-            for (; qi < e; ++qi) {
-                const ServeQuery& q = queries[R.order[qi]];
-                long len = long(q.suffix.size());
-                for (int t : q.tables) len += long(table_tokens_[size_t(t)].size());
-                if (M > 0 && M + len > kMaxRows) break;
-                R.window_of[qi] = int(wi);
-                sub_of[qi] = int(sub_end.size());
-                if (q.suffix.empty()) continue;
-                const int row0 = M;
-                int p = 0;
-                for (int t : q.tables) {
-                    for (int32_t tok : table_tokens_[size_t(t)]) {
-                        tokens.push_back(tok);
-                        group.push_back(group_of_[size_t(t)]);
-                        pos.push_back(p);
-                        pos64.push_back(p++);
-                    }
-                }
-                R.total_ctx_tokens += p;
-                for (int32_t tok : q.suffix) {
+    for (const auto& [qb, qe] : subs) {
+        std::vector<int32_t> tokens, pos, group, logit_rows;
+        std::vector<int64_t> pos64;
+        std::vector<AttnSeq> seqs;
+        std::vector<size_t> seq_query;
+        int M = 0;
+        for (size_t qi = qb; qi < qe; ++qi) {
+            const ServeQuery& q = queries[R.order[qi]];
+            R.window_of[qi] = int(qi / bc);
+            sub_of[qi] = int(sub_end.size());
+            if (q.suffix.empty()) continue;
+            const int row0 = M;
+            int p = 0;
+            for (int t : q.tables) {
+                for (int32_t tok : table_tokens_[size_t(t)]) {
                     tokens.push_back(tok);
-                    group.push_back(-1);
+                    group.push_back(group_of_[size_t(t)]);
                     pos.push_back(p);
                     pos64.push_back(p++);
                 }
-                M += p;
-                seqs.push_back({row0, p, 0, 0});
-                seq_query.push_back(qi);
-                logit_rows.push_back(M - 1);
             }
-            qb = qi;
-            R.total_suffix_tokens += M;
-            if (M > 0) {
-                StagingRing& ring = model_.ring();
-                FwdArgs fa;
-                fa.M = M;
-                fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
-                fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
-                fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
-                fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
-                fa.group_host = group.data();
-                fa.n_seqs = int(seqs.size());
-                fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
-                fa.seqs_host = seqs.data();
-                fa.mode = 1;
-                fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
-                fa.logit_rows_host = logit_rows.data();
-                fa.n_logit_rows = int(logit_rows.size());
-                fa.logits_out = d_logits;
-                fa.argmax_out = d_argmax + slot;
-                R.meta_bytes += tokens.size() * 20 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
-                model_.set_timing(opts.time_kernels);
-                model_.forward(fa, cs_);
-                R.launches += model_.launches();
-                if (opts.keep_logits) {
-                    for (size_t k = 0; k < seq_query.size(); ++k)
-                        TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
-                                                       sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
-                    TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
-                }
-                for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(slot + k);
-                slot += seq_query.size();
+            R.total_ctx_tokens += p;
+            for (int32_t tok : q.suffix) {
+                tokens.push_back(tok);
+                group.push_back(-1);
+                pos.push_back(p);
+                pos64.push_back(p++);
             }
-            sub_end.push_back(evp.get());
-            TKV_CUDA_CHECK(cudaEventRecord(sub_end.back(), cs_));
+            M += p;
+            seqs.push_back({row0, p, 0, 0});
+            seq_query.push_back(qi);
+            logit_rows.push_back(M - 1);
         }
-        win_end.push_back(sub_end.back());
+        R.total_suffix_tokens += M;
+        if (M > 0) {
+            StagingRing& ring = model_.ring();
+            FwdArgs fa;
+            fa.M = M;
+            fa.tokens = static_cast<const int32_t*>(ring.upload(tokens.data(), tokens.size() * 4, cs_));
+            fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, cs_));
+            fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, cs_));
+            fa.group = static_cast<const int32_t*>(ring.upload(group.data(), group.size() * 4, cs_));
+            fa.group_host = group.data();
+            fa.n_seqs = int(seqs.size());
+            fa.seqs = static_cast<const AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(AttnSeq), cs_));
+            fa.seqs_host = seqs.data();
+            fa.mode = 1;
+            fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
+            fa.logit_rows_host = logit_rows.data();
+            fa.n_logit_rows = int(logit_rows.size());
+            fa.logits_out = d_logits;
+            fa.argmax_out = d_argmax + qb;  // the k-th prefilling query of the sub-batch -> slot qb + k
+            R.meta_bytes += tokens.size() * 20 + seqs.size() * sizeof(AttnSeq) + logit_rows.size() * 4;
+            model_.set_timing(opts.time_kernels);
+            model_.forward(fa, cs_);
+            R.launches += model_.launches();
+            if (opts.keep_logits) {
+                for (size_t k = 0; k < seq_query.size(); ++k)
+                    TKV_CUDA_CHECK(cudaMemcpyAsync(logits_host.data() + seq_query[k] * vp, d_logits + k * vp,
+                                                   sizeof(float) * vp, cudaMemcpyDeviceToHost, cs_));
+                TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
+            }
+            for (size_t k = 0; k < seq_query.size(); ++k) R.argmax[seq_query[k]] = int32_t(qb + k);
+        }
+        sub_end.push_back(evp.get());
+        TKV_CUDA_CHECK(cudaEventRecord(sub_end.back(), cs_));
+        for (size_t qi = qb; qi < qe; ++qi) win_end[qi / bc] = sub_end.back();  // a window ends with its last sub-batch
     }
     R.host_ms = now_ms() - host0;
     TKV_CUDA_CHECK(cudaStreamSynchronize(cs_));
