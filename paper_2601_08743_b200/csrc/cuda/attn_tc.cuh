@@ -20,6 +20,13 @@ struct AttnArgs {
     __nv_bfloat16* out;          // [M][Hq*d]
     int num_heads, kv_heads, head_dim, mode;
     float scale;                 // 1/sqrt(d)
+    // paged V (tcgen05 kernel, cached prefix): when vpool is set, the V rows of cached-prefix
+    // tiles are copied straight from the table pages (the gather only materialises rotated K)
+    const uint8_t* vpool = nullptr;
+    int page_shift = 0, layer = 0, layers = 0;
+    const int32_t* page_ids = nullptr;   // window page-id list (GatherSeg::page_off indexes it)
+    const GatherSeg* segs = nullptr;     // window segments, ascending out_row0 (= ctx rows)
+    int n_segs = 0;
     const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row
                                       // (start of the row's group block; 0 for query rows)
 };

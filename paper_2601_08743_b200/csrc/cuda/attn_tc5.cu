@@ -220,7 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_ofree(st), 4);
         }
         for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), 1), mbar_init(b_kempty(i), 1);
-        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), 1), mbar_init(b_vempty(i), 1);
+        // V tiles come from the TMA lane (1 arrival) or, with paged V, from warps 2-3 (64 arrivals;
+        // for own-row tiles one of them arms the TMA transaction and the rest arrive plainly)
+        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), a.vpool ? 64 : 1), mbar_init(b_vempty(i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int h = 0; h < 2; ++h) tma_2d(dk + h * kKVHalf, ctx ? &mk_ctx : &mk_own, b_kfull(sk), it.kvh * D + h * 64, row);
                 }
             }
-        } else if (lane == 16) {  // ---- TMA: V tiles
+        } else if (lane == 16 && !a.vpool) {  // ---- TMA: V tiles
             long g = 0;
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
                 const Item it = item(w);
@@ -295,6 +297,59 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_expect_tx(b_vfull(sv), kKVTile);
                     for (int h = 0; h < 2; ++h) tma_2d(dv + h * kKVHalf, ctx ? &mv_ctx : &mv_own, b_vfull(sv), it.kvh * D + h * 64, row);
                 }
+            }
+        }
+    } else if ((warp == 2 || warp == 3) && a.vpool) {
+        // ---- paged V: cached-prefix tiles copied from the table pages with 16-byte cp.async into
+        // the swizzled tile (each of the 64 threads owns two key rows), own-row tiles by TMA
+        const int tid = threadIdx.x - 64;
+        const long row_bytes = long(a.kv_heads) * D * 2;
+        const long pmask = (1L << a.page_shift) - 1;
+        long g = 0;
+        for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
+            const Item it = item(w);
+            for (int t = 0; t < it.n_tiles; ++t, ++g) {
+                const int sv = int(g % kVStages);
+                mbar_wait(b_vempty(sv), int((g / kVStages) & 1) ^ 1);
+                bool ctx;
+                const int row = tile_row(it, t, ctx);
+                const uint32_t dv = s0 + kV0 + sv * kKVTile;
+                if (!ctx) {
+                    if (tid == 0) {
+                        mbar_expect_tx(b_vfull(sv), kKVTile);
+                        for (int h = 0; h < 2; ++h) tma_2d(dv + h * kKVHalf, &mv_own, b_vfull(sv), it.kvh * D + h * 64, row);
+                    } else {
+                        mbar_arrive(b_vfull(sv));
+                    }
+                    continue;
+                }
+                for (int rr = tid; rr < BN; rr += 64) {
+                    const int key = t * BN + rr;  // key index within this sequence's prefix
+                    if (key < it.sq.n_ctx) {
+                        const int vr = it.sq.ctx_row0 + key;  // window ctx row -> its table segment
+                        int lo = 0, hi = a.n_segs - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (a.segs[mid].out_row0 <= vr) lo = mid; else hi = mid - 1;
+                        }
+                        const GatherSeg sg = a.segs[lo];
+                        const long off = ((long(a.layers) + a.layer) * sg.tokens + (vr - sg.out_row0)) * row_bytes + long(it.kvh) * D * 2;
+                        const uint8_t* src = a.vpool + (long(a.page_ids[sg.page_off + (off >> a.page_shift)]) << a.page_shift) + (off & pmask);
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + c * 16) : "memory");
+                        }
+                    } else {  // past the prefix: finite zeros (masked in the softmax)
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(b_vfull(sv)) : "memory");
             }
         }
     } else if (warp == 1) {
@@ -337,7 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             auto pv = [&](const Cur& c, int st) {  // O_st += P_st . V(c), P_st from TMEM
                 const int sv = int(c.gi % kVStages);
-                if (st == 0) mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
+                if (st == 0) {
+                    mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
+                    if (a.vpool) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async rows -> tensor core
+                }
                 mbar_wait(b_pfull(st), int(c.gi & 1));
                 if (st == 0) TR(4, c.gi);
                 if (c.t == 0) mbar_wait(b_ofree(st), (c.j & 1) ^ 1);  // the previous item's epilogue read O_st

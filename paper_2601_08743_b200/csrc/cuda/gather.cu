@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(256) gather_rope_bf16_kernel(const uint8_t* __
         uint4 kv[2][4];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
+            if (c == 1 && !out_v) break;  // K only: the attention reads V from the pages
             const long base = ((long(c) * L + l) * sg.tokens + t) * row_in;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(256) gather_rope_bf16_kernel(const uint8_t* __
             }
             const long o = (long(sg.out_row0 + t) * kvdim + long(vi) * 8) * 2;
             *reinterpret_cast<uint4*>(out_k + o) = w;
-            *reinterpret_cast<uint4*>(out_v + o) = kv[1][q];
+            if (out_v) *reinterpret_cast<uint4*>(out_v + o) = kv[1][q];
         }
     }
 }
@@ -209,8 +210,9 @@ __global__ void __launch_bounds__(256) gather_rope_tma_kernel(const uint8_t* __r
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * run) : "memory");
-        for (int kv = 0; kv < 2; ++kv) {
+        const int n_kv = out_v ? 2 : 1;  // K only when the attention reads V from the pages itself
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n_kv * run) : "memory");
+        for (int kv = 0; kv < n_kv; ++kv) {
             long off = ((long(kv) * L + l) * sg.tokens + ch.y) * row_bytes;
             uint32_t dst = kv ? s_v : s_k, left = run;
             while (left) {  // split the run at page boundaries
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(256) gather_rope_tma_kernel(const uint8_t* __r
     if (threadIdx.x == 0) {
         const long o = long(sg.out_row0 + ch.y) * row_bytes;
         bulk_s2g(out_k + o, s_k, run);
-        bulk_s2g(out_v + o, s_v, run);
+        if (out_v) bulk_s2g(out_v + o, s_v, run);
         asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     __syncthreads();

@@ -270,6 +270,9 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         if (contiguous) d_row_lo = static_cast<const int32_t*>(ring_.upload(lo.data(), lo.size() * 4, s));
     }
     const bool use_tc5 = attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0 && (a.mode == 0 || d_row_lo != nullptr);
+    // paged V needs the tcgen05 kernel, the bf16 TMA gather (K only) and power-of-two pages
+    const bool paged_v = a.paged_v && use_tc5 && a.mode == 0 && a.gather_segs && a.gather_chunks &&
+                         a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1));
     const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
@@ -334,7 +337,8 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             if (a.gather_chunks && a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1)))
                 launch_gather_rope_bf16(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_chunks,
                                         a.gather_n_chunks, c.num_layers, l, kvd, c.head_dim, rope_.cos_f(), rope_.sin_f(),
-                                        const_cast<void*>(a.ctx_k), const_cast<void*>(a.ctx_v), a.ctx_rows, s);
+                                        const_cast<void*>(a.ctx_k), paged_v ? nullptr : const_cast<void*>(a.ctx_v),
+                                        a.ctx_rows, s);
             else
                 launch_gather_rope(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_n_segs,
                                    a.gather_rows, c.num_layers, kvd, c.head_dim, a.gather_in, DType::bf16, rope_.cos_d(),
@@ -359,6 +363,17 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.mode = a.mode;
         aa.scale = float(1.0 / std::sqrt(double(c.head_dim)));
         aa.row_lo = d_row_lo;
+        if (paged_v) {
+            aa.vpool = a.gather_pool;
+            int sh = 0;
+            while ((size_t(1) << sh) < a.gather_page_bytes) ++sh;
+            aa.page_shift = sh;
+            aa.page_ids = a.gather_pages;
+            aa.segs = a.gather_segs;
+            aa.n_segs = a.gather_n_segs;
+            aa.layer = l;
+            aa.layers = c.num_layers;
+        }
         {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing_) {

@@ -562,6 +562,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 fa.gather_in = in_dt_s;
                 fa.gather_chunks = d_chunks_s;
                 fa.gather_n_chunks = n_chunks_s;
+                static const bool paged_v = [] {  // TKV_PAGED_V=0 keeps V in the gathered slab (A/B)
+                    const char* e = std::getenv("TKV_PAGED_V");
+                    return !(e && std::string(e) == "0");
+                }();
+                fa.paged_v = paged_v;
             }
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
             fa.logit_rows_host = logit_rows.data();
