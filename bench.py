@@ -346,11 +346,12 @@ def main():
     nc_n = min(args.nocache_queries, n_local)
     sl = my_slice(global_order())[:nc_n]
     qs_nc = [(analyzed[i]["assembly_order"], analyzed[i]["remainder"]) for i in sl]
-    nc_opts = N.serve_options(rerank_on=0, capacity=args.capacity, b_c=args.b_c, b_m=args.b_m, nocache=1)
-    store.serve(qs_nc, nc_opts)  # warm-up
-    nc = store.serve(qs_nc, nc_opts)
-    cached_sub = store.serve(qs_nc, N.serve_options(rerank_on=0, capacity=args.capacity, policy=args.policy, b_c=args.b_c,
-                                                    b_m=args.b_m))
+    if nc_n:
+        nc_opts = N.serve_options(rerank_on=0, capacity=args.capacity, b_c=args.b_c, b_m=args.b_m, nocache=1)
+        store.serve(qs_nc, nc_opts)  # warm-up
+        nc = store.serve(qs_nc, nc_opts)
+        cached_sub = store.serve(qs_nc, N.serve_options(rerank_on=0, capacity=args.capacity, policy=args.policy,
+                                                        b_c=args.b_c, b_m=args.b_m))
     # ---- e2e: prompt text in, first tokens out, through the C ABI (wall clock)
     # the user path: the rank's prompts in arrival order; serve_text reranks them itself
     e2e_texts = [entries[i][1] for i in sorted(my_slice(global_order()))]
@@ -391,7 +392,7 @@ def main():
                    else cpu_baseline_sample(eng, entries, n=8))
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unavailable": str(e)}
-    nc_p50, c_p50 = pct(nc["ttft_ms"], 0.5), pct(cached_sub["ttft_ms"], 0.5)
+    nc_p50, c_p50 = (pct(nc["ttft_ms"], 0.5), pct(cached_sub["ttft_ms"], 0.5)) if nc_n else (None, None)
     line = {
         "metric": "prefill queries/sec (cached path); p50/p99 TTFT vs no-cache prefill; KV load GB/s vs PCIe",
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -413,7 +414,8 @@ def main():
                     "qps": nc_n / (nc["makespan_ms"] / 1e3), "cached_p50_ttft_ms_same_subset": c_p50,
                     "cached_qps_same_subset": nc_n / (cached_sub["makespan_ms"] / 1e3),
                     "p50_ttft_reduction": nc_p50 / c_p50 if c_p50 else None,
-                    "argmax_agreement": float(np.mean([a == b for a, b in zip(nc["argmax"], cached_sub["argmax"])]))},
+                    "argmax_agreement": float(np.mean([a == b for a, b in zip(nc["argmax"], cached_sub["argmax"])]))}
+                   if nc_n else {"queries": 0},
         "kv_load": {"bytes_per_step": h2d, "copy_busy_ms_per_step": copy_ms,
                     "demand_bytes_per_step": dem_b, "demand_copy_ms_per_step": dem_ms,
                     "gbs": dem_b / (dem_ms / 1e3) / 1e9 if dem_ms else None, "pcie_h2d_peak_gbs": pcie,

@@ -27,6 +27,7 @@ struct AttnArgs {
     const int32_t* page_ids = nullptr;   // window page-id list (GatherSeg::page_off indexes it)
     const GatherSeg* segs = nullptr;     // window segments, ascending out_row0 (= ctx rows)
     int n_segs = 0;
+    int prefetch = 0;                    // tiles ahead pulled into L2 (0 = off)
     const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row
                                       // (start of the row's group block; 0 for query rows)
 };

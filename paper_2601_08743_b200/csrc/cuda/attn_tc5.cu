@@ -36,7 +36,13 @@ namespace {
 
 constexpr int BM = 128, BN = 128, D = 128;
 constexpr int kThreads = 384;  // warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); warpgroups 1 / 2: softmax of Q0 / Q1
-constexpr int kKStages = 2, kVStages = 2;
+#ifndef TKV_ATTN_KSTAGES
+#define TKV_ATTN_KSTAGES 2
+#endif
+#ifndef TKV_ATTN_VSTAGES
+#define TKV_ATTN_VSTAGES 2
+#endif
+constexpr int kKStages = TKV_ATTN_KSTAGES, kVStages = TKV_ATTN_VSTAGES;
 constexpr int kQHalf = BM * 64 * 2;        // Q tile: two [128 rows][64 dims] SW128 blocks, 16 KB each
 constexpr int kQTile = 2 * kQHalf;         // 32 KB; one per stream
 constexpr int kKVHalf = BN * 64 * 2;       // K/V tile: two [128 keys][64 dims] SW128 blocks, 16 KB each
@@ -48,6 +54,7 @@ constexpr int kBarOff = kV0 + kVStages * kKVTile;
 constexpr int kStreamBars = 4;
 constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
+static_assert(kSmem <= 227 * 1024, "attention smem over the per-CTA limit");
 // TMEM columns: S_s (f32, P_s as packed bf16 over its first 64 columns) at 128 s, O_s at 256 + 128 s
 constexpr int kTmemCols = 512;
 
@@ -73,6 +80,15 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint3
     asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
                  "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y)
                  : "memory");
+}
+// L2 prefetch of a future tile (no smem, no barrier): the rings are 2 deep, so a tile's HBM latency
+// under load (several us with K and V streaming on every SM) is hidden by pulling it into L2 early
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -272,7 +288,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                it.sq.q_row0 + it.tok0 + st * TQ);
                 }
                 TR(8, j);
+                auto prefetch_kv = [&](int t) {  // K always; V here only when it comes by TMA
+                    bool ctx;
+                    const int row = tile_row(it, t, ctx);
+                    for (int h = 0; h < 2; ++h) {
+                        tma_prefetch_2d(ctx ? &mk_ctx : &mk_own, it.kvh * D + h * 64, row);
+                        if (!a.vpool || !ctx) tma_prefetch_2d(ctx ? &mv_ctx : &mv_own, it.kvh * D + h * 64, row);
+                    }
+                };
+                const int pf = a.prefetch;
+                for (int t = kKStages; t < min(pf, it.n_tiles); ++t) prefetch_kv(t);
                 for (int t = 0; t < it.n_tiles; ++t, ++g) {
+                    if (pf && t + pf < it.n_tiles) prefetch_kv(t + pf);
                     const int sk = int(g % kKStages);
                     mbar_wait(b_kempty(sk), int((g / kKStages) & 1) ^ 1);
                     TR(0, g);
@@ -305,12 +332,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tid = threadIdx.x - 64;
         const long row_bytes = long(a.kv_heads) * D * 2;
         const long pmask = (1L << a.page_shift) - 1;
+        // The V row of prefix key `key` inside its table's pages. Keys only grow along a CTA's walk
+        // through an item, so each lookup advances a per-thread segment cursor (one binary search
+        // per item) and remembers the last page, instead of searching per row.
+        struct VCur {
+            int seg, next_row0;  // current segment; first row of the next one (INT_MAX past the end)
+            GatherSeg sg;
+        };
+        auto v_seek = [&](VCur& c, int vr) {  // binary search: the segment holding window row vr
+            int lo = 0, hi = a.n_segs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (a.segs[mid].out_row0 <= vr) lo = mid; else hi = mid - 1;
+            }
+            c.seg = lo;
+            c.sg = a.segs[lo];
+            c.next_row0 = lo + 1 < a.n_segs ? a.segs[lo + 1].out_row0 : 0x7fffffff;
+        };
+        auto v_src = [&](VCur& c, const Item& it, int key) {
+            const int vr = it.sq.ctx_row0 + key;  // window ctx row -> its table segment
+            while (vr >= c.next_row0) {
+                ++c.seg;
+                c.sg = a.segs[c.seg];
+                c.next_row0 = c.seg + 1 < a.n_segs ? a.segs[c.seg + 1].out_row0 : 0x7fffffff;
+            }
+            const long off = ((long(a.layers) + a.layer) * c.sg.tokens + (vr - c.sg.out_row0)) * row_bytes + long(it.kvh) * D * 2;
+            return a.vpool + (long(__ldg(a.page_ids + c.sg.page_off + (off >> a.page_shift))) << a.page_shift) + (off & pmask);
+        };
+        const int pf = a.prefetch;
+        VCur cl, cp;  // load cursor, prefetch cursor
+        auto prefetch_v = [&](const Item& it, int t) {
+            if (t >= it.n_ctx_tiles) return;  // own tiles: the TMA lane prefetches them
+            for (int rr = tid; rr < BN; rr += 64)
+                if (t * BN + rr < it.sq.n_ctx) bulk_prefetch(v_src(cp, it, t * BN + rr), D * 2);
+        };
         long g = 0;
         for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
             const Item it = item(w);
+            if (it.n_ctx_tiles) {
+                v_seek(cl, it.sq.ctx_row0);
+                cp = cl;
+            }
+            for (int t = kVStages; t < min(pf, it.n_tiles); ++t) prefetch_v(it, t);
             for (int t = 0; t < it.n_tiles; ++t, ++g) {
+                if (pf && t + pf < it.n_tiles) prefetch_v(it, t + pf);
                 const int sv = int(g % kVStages);
                 mbar_wait(b_vempty(sv), int((g / kVStages) & 1) ^ 1);
+                if (tid == 0) TR(1, g);
                 bool ctx;
                 const int row = tile_row(it, t, ctx);
                 const uint32_t dv = s0 + kV0 + sv * kKVTile;
@@ -326,15 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int rr = tid; rr < BN; rr += 64) {
                     const int key = t * BN + rr;  // key index within this sequence's prefix
                     if (key < it.sq.n_ctx) {
-                        const int vr = it.sq.ctx_row0 + key;  // window ctx row -> its table segment
-                        int lo = 0, hi = a.n_segs - 1;
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (a.segs[mid].out_row0 <= vr) lo = mid; else hi = mid - 1;
-                        }
-                        const GatherSeg sg = a.segs[lo];
-                        const long off = ((long(a.layers) + a.layer) * sg.tokens + (vr - sg.out_row0)) * row_bytes + long(it.kvh) * D * 2;
-                        const uint8_t* src = a.vpool + (long(a.page_ids[sg.page_off + (off >> a.page_shift)]) << a.page_shift) + (off & pmask);
+                        const uint8_t* src = v_src(cl, it, key);
 #pragma unroll
                         for (int c = 0; c < 16; ++c) {
                             const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
@@ -394,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int sv = int(c.gi % kVStages);
                 if (st == 0) {
                     mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
+                    TR(11, c.gi);
                     if (a.vpool) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async rows -> tensor core
                 }
                 mbar_wait(b_pfull(st), int(c.gi & 1));

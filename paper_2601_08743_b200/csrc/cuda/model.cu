@@ -363,6 +363,11 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.mode = a.mode;
         aa.scale = float(1.0 / std::sqrt(double(c.head_dim)));
         aa.row_lo = d_row_lo;
+        static const int attn_prefetch = [] {  // L2 prefetch distance of the tcgen05 attention's K/V tiles
+            const char* e = std::getenv("TKV_ATTN_PREFETCH");
+            return e ? std::atoi(e) : 0;
+        }();
+        aa.prefetch = attn_prefetch;
         if (paged_v) {
             aa.vpool = a.gather_pool;
             int sh = 0;

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtkv.so")
+LIB_PATH = os.environ.get("TKV_LIB") or os.path.join(_HERE, "lib", "libtkv.so")  # TKV_LIB: A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libtkv.so not built: run `make -C paper_2601_08743_b200` (or __graft_entry__.build())")
