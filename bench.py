@@ -441,7 +441,7 @@ def main():
                    "gbs": (sum(r["gather_bytes"] for r in results) / (sum(r["gather_ms"] for r in results) / 1e3) / 1e9
                            if sum(r["gather_ms"] for r in results) else None),
                    "peak_gbs": peaks.get("hbm_gbs"),
-                   "bytes_definition": "prefix rows x 2 (K,V) x layers x kv_dim x (read + write element bytes)"},
+                   "bytes_definition": "prefix rows x layers x kv_dim x (read + write element bytes) for K (rotated into the slab); V is read by the attention straight from the pages (paged V; TKV_PAGED_V=0 gathers V too and counts it)"},
         "global_rerank_ms_per_step": sum(timed_rerank_ms) / args.steps,
         "attention_ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
         "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,

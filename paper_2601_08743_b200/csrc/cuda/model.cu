@@ -203,17 +203,17 @@ cudaEvent_t Model::timing_event() {
 }
 
 void Model::add_timed(cudaEvent_t a, cudaEvent_t b, double flops) {
-    timed_.push_back({a, b, flops < 0 ? 0.0 : flops, flops < 0 ? 2 : (flops == 0 ? 1 : 0)});
+    timed_.push_back({a, b, flops < 0 ? -flops : flops, flops < 0 ? 2 : (flops == 0 ? 1 : 0)});
 }
 
-void Model::collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms) {
-    gemm_ms = gemm_flops = gather_ms = attn_ms = 0;
+void Model::collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms, double& gather_bytes) {
+    gemm_ms = gemm_flops = gather_ms = attn_ms = gather_bytes = 0;
     for (const TimedRec& r : timed_) {
         float ms = 0;
         TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
         if (r.kind == 0) gemm_ms += ms, gemm_flops += r.flops;
         else if (r.kind == 1) attn_ms += ms;
-        else gather_ms += ms;
+        else gather_ms += ms, gather_bytes += r.flops;
     }
     timed_.clear();
     ev_used_ = 0;
@@ -347,7 +347,9 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             ++nl;
             if (timing_) {
                 TKV_CUDA_CHECK(cudaEventRecord(e1, s));
-                add_timed(e0, e1, -1.0);
+                // algorithmic bytes: each prefix row's K (and V unless paged) read from the pages + written
+                const double in_b = a.gather_in == DType::bf16 ? 2.0 : 4.0;
+                add_timed(e0, e1, -double(a.ctx_rows) * kvd * (paged_v ? 1 : 2) * (in_b + 2.0));
             }
         }
         const size_t ctx_off = streamed ? 0 : size_t(l) * a.ctx_rows * kvd * 2;

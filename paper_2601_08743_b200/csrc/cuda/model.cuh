@@ -139,8 +139,8 @@ class Model {
     // attention kernel: 0 = tcgen05 where supported (head_dim 128), 1 = mma.sync everywhere
     void set_attention_impl(int impl) { attn_impl_ = impl; }
     int attention_impl() const { return attn_impl_; }
-    void add_timed(cudaEvent_t a, cudaEvent_t b, double flops);  // flops < 0 tags a gather
-    void collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms);
+    void add_timed(cudaEvent_t a, cudaEvent_t b, double flops);  // flops < 0 tags a gather moving -flops bytes
+    void collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms, double& gather_bytes);
     cudaEvent_t timing_event();
 
    private:

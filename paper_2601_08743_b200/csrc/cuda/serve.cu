@@ -517,7 +517,6 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             d_chunks_s = static_cast<const int4*>(ring.upload(chunks.data(), chunks.size() * sizeof(int4), cs_));
             R.meta_bytes += chunks.size() * sizeof(int4);
             R.meta_bytes += segs.size() * sizeof(GatherSeg) + page_ids.size() * 4;
-            if (opts.time_kernels) R.gather_bytes += double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt_s) + oes);
         } else if (ctx_rows > 0 && !stream_ctx) {
             auto* d_segs = static_cast<GatherSeg*>(ring.upload(segs.data(), segs.size() * sizeof(GatherSeg), cs_));
             auto* d_pages = static_cast<int32_t*>(ring.upload(page_ids.data(), page_ids.size() * 4, cs_));
@@ -535,8 +534,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             R.launches += 1;
             if (opts.time_kernels) {
                 TKV_CUDA_CHECK(cudaEventRecord(g1, cs_));
-                R.gather_bytes += double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt) + oes);
-                model_.add_timed(g0, g1, -1.0);  // tagged gather
+                model_.add_timed(g0, g1, -double(ctx_rows) * 2 * L * kvd * (dtype_size(in_dt) + oes));  // tagged gather
             }
         }
         if (M > 0) {
@@ -642,7 +640,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         R.copy_demand_ms += d;
         R.copy_busy_ms += d + elapsed(pspan[i].first, pspan[i].second);
     }
-    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
+    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms, R.gather_bytes);
     if (opts.keep_logits) R.logits = std::move(logits_host);
     R.wall_ms = now_ms() - host0;
     if (host_prof)
@@ -794,7 +792,7 @@ ServeResult Server::serve_nocache(const std::vector<ServeQuery>& queries, const 
     R.ttft_ms.resize(n);
     for (size_t qi = 0; qi < n; ++qi) R.ttft_ms[qi] = elapsed(t0, sub_end[size_t(sub_of[qi])]);
     R.makespan_ms = R.window_end_ms.back();
-    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms);
+    if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms, R.gather_bytes);
     if (opts.keep_logits) R.logits = std::move(logits_host);
     return R;
 }

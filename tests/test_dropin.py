@@ -32,6 +32,13 @@ def _run(args, timeout=900):
 @pytest.mark.parametrize("suite", HOST_SUITES)
 def test_reference_unit_suite_passes_against_b200_build(suite):
     rc, out = _run([UNIT, "-ts=" + suite])
+    # wall-clock assertions in the reference suite (schema_test.cpp:346, graph build "scales
+    # near-linearly") flake on a loaded shared host: only those may be retried, twice
+    for _ in range(2):
+        failed = [ln for ln in out.splitlines() if ": FAILED in " in ln or ": ERROR in " in ln]
+        if rc == 0 or not failed or not all("scales near-linearly" in ln for ln in failed):
+            break
+        rc, out = _run([UNIT, "-ts=" + suite])
     assert rc == 0 and "0 failed" in out, out[-3000:]
     assert "test cases: 0 " not in out
 
