@@ -138,6 +138,36 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
                  : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// pins registers filled by an asynchronous tcgen05.ld after the wait that completes it (the
+// compiler cannot hoist their uses above this volatile asm)
+__device__ __forceinline__ void reg_fence32(uint32_t* v) {
+    asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]), "+r"(v[8]),
+                 "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]),
+                 "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), "+r"(v[24]),
+                 "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31]));
+}
+// packed f32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per instruction)
+__device__ __forceinline__ uint64_t pack_f32x2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t pack_u32x2(uint32_t a, uint32_t b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ void unpack_f32x2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -520,23 +550,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(b_sfull(st), int(gi & 1));
                 if (warp == 4 && lane == 0) TR(5, gi);
                 fence_after();
-                uint32_t u[BN];
+                // S is read from TMEM twice, 32 columns at a time with the next chunk's load in flight:
+                // pass 1 takes the row max, pass 2 the exponentials. Two 32-register chunks instead of
+                // the whole 128-column row keep the softmax warps far from their register cap.
+                const bool masked = !(ctx && base_j + BN <= sq.n_ctx);  // full prefix tiles skip the mask
+                const int lim = masked ? min(seg_end, causal + 1) - base_j : BN;  // columns [lo_c, lim) visible
+                const int lo_c = masked ? lo - base_j : 0;
+                auto mask_chunk = [&](uint32_t* v, int c0) {
+                    if (masked) {
 #pragma unroll
-                for (int c = 0; c < BN; c += 32) tmem_ld32_async(tS + c, u + c);
+                        for (int i = 0; i < 32; ++i)
+                            if (c0 + i >= lim || c0 + i < lo_c) v[i] = 0xff800000u;  // -inf
+                    }
+                };
+                uint32_t ua[32], ub[32];
+                // row max as four independent 3-input max chains (FMNMX3)
+                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                auto max_chunk = [&](const uint32_t* v) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            m4[q] = fmaxf(fmaxf(m4[q], __uint_as_float(v[i + 2 * q])), __uint_as_float(v[i + 2 * q + 1]));
+                };
+                tmem_ld32_async(tS, ua);
                 tmem_wait_ld();
-                float mx = -INFINITY;
-                if (ctx && base_j + BN <= sq.n_ctx) {  // full prefix tile: nothing masked
+                reg_fence32(ua);
+                if (warp == 4 && lane == 0) TR(12, gi);
 #pragma unroll
-                    for (int c = 0; c < BN; ++c) mx = fmaxf(mx, __uint_as_float(u[c]));
-                } else {
-                    const int lim = min(seg_end, causal + 1) - base_j;  // columns [lo_c, lim) visible
-                    const int lo_c = lo - base_j;
-#pragma unroll
-                    for (int c = 0; c < BN; ++c) {
-                        if (c >= lim || c < lo_c) u[c] = 0xff800000u;  // -inf
-                        mx = fmaxf(mx, __uint_as_float(u[c]));
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t* cur = (k & 1) ? ub : ua;
+                    uint32_t* nxt = (k & 1) ? ua : ub;
+                    if (k < 3) tmem_ld32_async(tS + 32 * (k + 1), nxt);
+                    mask_chunk(cur, 32 * k);
+                    max_chunk(cur);
+                    if (k < 3) {
+                        tmem_wait_ld();
+                        reg_fence32(nxt);
                     }
                 }
+                float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 mx *= sl2;  // scale > 0: the max commutes with it
                 // conditional rescale: keep the running max unless it grows by more than 8 (x256)
                 const bool grow = mx > m_run + 8.f;
@@ -555,22 +608,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (grow) l_run *= corr;
                 }
                 if (grow) m_run = mx;
-                const float nb = m_run == -INFINITY ? 0.f : -m_run;
-                // P -> bf16 pairs over S's first 64 columns (this thread's row only)
-                float sum = 0.f;
+                if (warp == 4 && lane == 0) TR(13, gi);
+                // rows past the item's tokens get P = 0 through the bias (-inf)
+                const float nb = !live ? -INFINITY : (m_run == -INFINITY ? 0.f : -m_run);
+                // pass 2: x*scale*log2e - m on column pairs (FFMA2), exp2 on the MUFU, row sum in two
+                // packed accumulators (FADD2), P as bf16 pairs over S's first 64 columns (chunk k's P
+                // lands on columns [16k, 16k+16), all of which pass 2 has already read)
+                const uint64_t sl2x2 = pack_f32x2(sl2, sl2), nbx2 = pack_f32x2(nb, nb);
+                uint64_t acc[2] = {0ull, 0ull};
+                tmem_ld32_async(tS, ua);
+                tmem_wait_ld();
+                reg_fence32(ua);
 #pragma unroll
-                for (int c = 0; c < BN; c += 32) {
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t* cur = (k & 1) ? ub : ua;
+                    uint32_t* nxt = (k & 1) ? ua : ub;
+                    if (k < 3) tmem_ld32_async(tS + 32 * (k + 1), nxt);
+                    mask_chunk(cur, 32 * k);
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
-                        const float p0 = live ? ex2(fmaf(__uint_as_float(u[c + i]), sl2, nb)) : 0.f;
-                        const float p1 = live ? ex2(fmaf(__uint_as_float(u[c + i + 1]), sl2, nb)) : 0.f;
-                        sum += p0 + p1;
+                        float a0, a1;
+                        unpack_f32x2(ffma2(pack_u32x2(cur[i], cur[i + 1]), sl2x2, nbx2), a0, a1);
+                        const float p0 = ex2(a0), p1 = ex2(a1);
+#ifdef TKV_ATTN_PTRUNC
+                        // bf16 P by truncation (one PRMT per pair on the ALU instead of an F2FP), and
+                        // the row sum over the same truncated values so O / l stays consistent
+                        const uint32_t b0 = __float_as_uint(p0) & 0xffff0000u, b1 = __float_as_uint(p1) & 0xffff0000u;
+                        acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], pack_u32x2(b0, b1));
+                        pk[i >> 1] = __byte_perm(b0, b1, 0x7632);
+#else
+                        acc[(i >> 1) & 1] = fadd2(acc[(i >> 1) & 1], pack_f32x2(p0, p1));
                         pk[i >> 1] = pack_bf16x2(p0, p1);
+#endif
                     }
-                    tmem_st16(tS + (c >> 1), pk);
+                    tmem_st16(tS + 16 * k, pk);
+                    if (k < 3) {
+                        tmem_wait_ld();
+                        reg_fence32(nxt);
+                    }
                 }
-                l_run += sum;
+                float s0, s1, s2, s3;
+                unpack_f32x2(acc[0], s0, s1);
+                unpack_f32x2(acc[1], s2, s3);
+                l_run += (s0 + s1) + (s2 + s3);
+                if (warp == 4 && lane == 0) TR(14, gi);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
                 __syncwarp();
