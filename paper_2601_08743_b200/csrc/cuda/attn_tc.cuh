@@ -28,6 +28,7 @@ struct AttnArgs {
     const GatherSeg* segs = nullptr;     // window segments, ascending out_row0 (= ctx rows)
     int n_segs = 0;
     int prefetch = 0;                    // tiles ahead pulled into L2 (0 = off)
+    long k_hm_rows = 0;                  // > 0: k_ctx is head-major [kv head][k_hm_rows][head_dim]
     const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row
                                       // (start of the row's group block; 0 for query rows)
 };

@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     bool ctx;
                     const int row = tile_row(it, t, ctx);
                     for (int h = 0; h < 2; ++h) {
-                        tma_prefetch_2d(ctx ? &mk_ctx : &mk_own, it.kvh * D + h * 64, row);
+                        const bool hm = ctx && a.k_hm_rows;
+                        tma_prefetch_2d(ctx ? &mk_ctx : &mk_own, hm ? h * 64 : it.kvh * D + h * 64, hm ? int(it.kvh * a.k_hm_rows) + row : row);
                         if (!a.vpool || !ctx) tma_prefetch_2d(ctx ? &mv_ctx : &mv_own, it.kvh * D + h * 64, row);
                     }
                 };
@@ -337,7 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int row = tile_row(it, t, ctx);
                     const uint32_t dk = s0 + kK0 + sk * kKVTile;
                     mbar_expect_tx(b_kfull(sk), kKVTile);
-                    for (int h = 0; h < 2; ++h) tma_2d(dk + h * kKVHalf, ctx ? &mk_ctx : &mk_own, b_kfull(sk), it.kvh * D + h * 64, row);
+                    const bool hm = ctx && a.k_hm_rows;  // head-major slab: the head's block, rows within it
+                    for (int h = 0; h < 2; ++h)
+                        tma_2d(dk + h * kKVHalf, ctx ? &mk_ctx : &mk_own, b_kfull(sk), hm ? h * 64 : it.kvh * D + h * 64,
+                               hm ? int(it.kvh * a.k_hm_rows) + row : row);
                 }
             }
         } else if (lane == 16 && !a.vpool) {  // ---- TMA: V tiles
@@ -747,7 +751,8 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
         attr = true;
     }
     const int kvd = a.kv_heads * D;
-    const CUtensorMap mkc = rows_map(a.k_ctx, ctx_rows, kvd), mvc = rows_map(a.v_ctx, ctx_rows, kvd);
+    const CUtensorMap mkc = a.k_hm_rows ? rows_map(a.k_ctx, a.k_hm_rows * a.kv_heads, D) : rows_map(a.k_ctx, ctx_rows, kvd);
+    const CUtensorMap mvc = rows_map(a.v_ctx, ctx_rows, kvd);
     const CUtensorMap mko = rows_map(a.k_own, own_rows, kvd), mvo = rows_map(a.v_own, own_rows, kvd);
     const CUtensorMap mq = q_map(a.q, own_rows, a.num_heads, a.num_heads / a.kv_heads);
     static const char* trace_path = std::getenv("TKV_ATTN_TRACE");

@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(256) gather_rope_tma_kernel(const uint8_t* __r
                                                               const GatherSeg* __restrict__ segs, const int4* __restrict__ chunks,
                                                               int L, int l, int kvdim, int head_dim,
                                                               const float* __restrict__ cos_f, const float* __restrict__ sin_f,
-                                                              uint8_t* __restrict__ out_k, uint8_t* __restrict__ out_v) {
+                                                              uint8_t* __restrict__ out_k, uint8_t* __restrict__ out_v,
+                                                              long hm_rows) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     const int4 ch = chunks[blockIdx.x];  // {seg, t0, rows, 0}
@@ -233,6 +234,27 @@ __global__ void __launch_bounds__(256) gather_rope_tma_kernel(const uint8_t* __r
                          : "memory");
     }
     const int vpr = kvdim >> 3, half = head_dim >> 1;
+    if (hm_rows) {  // head-major K: rotate in registers and store each 16-byte vector straight to its head's block
+        for (int i = threadIdx.x; i < ch.z * vpr; i += blockDim.x) {
+            const int r = i / vpr, vi = i - r * vpr;
+            const long pos = sg.pos0 + ch.y + r;
+            uint4 w = *reinterpret_cast<const uint4*>(sm + long(r) * row_bytes + vi * 16);
+            const int e0 = vi * 8, hh = e0 / head_dim, d0 = e0 - hh * head_dim;
+            if (pos != 0) {
+                const float4 c = *reinterpret_cast<const float4*>(cos_f + pos * half + (d0 >> 1));
+                const float4 sn = *reinterpret_cast<const float4*>(sin_f + pos * half + (d0 >> 1));
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+                const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 ab = unpack_bf16x2(wp[e]);
+                    wp[e] = pack_bf16x2(fmaf(ab.x, cc[e], -ab.y * ss[e]), fmaf(ab.x, ss[e], ab.y * cc[e]));
+                }
+            }
+            *reinterpret_cast<uint4*>(out_k + ((long(hh) * hm_rows + sg.out_row0 + ch.y + r) * head_dim + d0) * 2) = w;
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < ch.z * vpr; i += blockDim.x) {
         const int r = i / vpr, vi = i - r * vpr;
         const long pos = sg.pos0 + ch.y + r;
@@ -283,8 +305,9 @@ int gather_chunks(const GatherSeg* segs, int n_segs, std::vector<int4>& out) {
 
 void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
                              const int4* d_chunks, int n_chunks, int L, int l, int kvdim, int head_dim, const float* cos_f,
-                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s) {
+                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s, bool k_head_major) {
     if (n_chunks <= 0) return;
+    if (k_head_major && (out_v || !gather_use_tma())) throw std::invalid_argument("gather: head-major K needs the TMA kernel, K only");
     if (kvdim % 8 || head_dim % 8) throw std::invalid_argument("gather: kv row must hold whole 16-byte vectors");
     if (page_bytes & (page_bytes - 1)) throw std::invalid_argument("gather fast path: page size must be a power of two");
     int shift = 0;
@@ -297,7 +320,8 @@ void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32
             attr = true;
         }
         gather_rope_tma_kernel<<<n_chunks, 256, smem, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim, head_dim,
-                                                           cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v));
+                                                           cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v),
+                                                           k_head_major ? out_rows : 0L);
     } else {
         gather_rope_bf16_kernel<<<n_chunks, 32 * kChunkRows, 0, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim,
                                                                      head_dim, cos_f, sin_f, static_cast<uint8_t*>(out_k),

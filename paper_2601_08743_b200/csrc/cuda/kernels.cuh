@@ -52,7 +52,10 @@ void launch_gather_rope(const uint8_t* pool, size_t page_bytes, const int32_t* d
 int gather_chunks(const GatherSeg* segs, int n_segs, std::vector<int4>& out);
 void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32_t* d_page_ids, const GatherSeg* d_segs,
                              const int4* d_chunks, int n_chunks, int L, int l, int kvdim, int head_dim, const float* cos_f,
-                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s);
+                             const float* sin_f, void* out_k, void* out_v, long out_rows, cudaStream_t s, bool k_head_major = false);
+// k_head_major (K only, out_v null): out_k is [kv head][out_rows][head_dim], so one kv head's
+// 128-key tile is a contiguous 32 KB block for the attention's TMA.
+bool gather_use_tma();
 // (l0, nl): gather only layers [l0, l0 + nl) of the L-layer images into out layers [0, nl) — the
 // serving path streams one layer of prefix at a time just before that layer's attention.
 

@@ -273,6 +273,12 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
     // paged V needs the tcgen05 kernel, the bf16 TMA gather (K only) and power-of-two pages
     const bool paged_v = a.paged_v && use_tc5 && a.mode == 0 && a.gather_segs && a.gather_chunks &&
                          a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1));
+    // with paged V the K slab is written head-major (one kv head's key tile = one contiguous block)
+    static const bool hm_env = [] {
+        const char* e = std::getenv("TKV_K_HEAD_MAJOR");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool k_head_major = paged_v && hm_env && gather_use_tma();
     const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
@@ -338,7 +344,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
                 launch_gather_rope_bf16(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_chunks,
                                         a.gather_n_chunks, c.num_layers, l, kvd, c.head_dim, rope_.cos_f(), rope_.sin_f(),
                                         const_cast<void*>(a.ctx_k), paged_v ? nullptr : const_cast<void*>(a.ctx_v),
-                                        a.ctx_rows, s);
+                                        a.ctx_rows, s, k_head_major);
             else
                 launch_gather_rope(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_n_segs,
                                    a.gather_rows, c.num_layers, kvd, c.head_dim, a.gather_in, DType::bf16, rope_.cos_d(),
@@ -370,6 +376,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             return e ? std::atoi(e) : 0;
         }();
         aa.prefetch = attn_prefetch;
+        if (k_head_major) aa.k_hm_rows = a.ctx_rows;
         if (paged_v) {
             aa.vpool = a.gather_pool;
             int sh = 0;
