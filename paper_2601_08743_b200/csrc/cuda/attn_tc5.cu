@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float a0, a1;
                         unpack_f32x2(ffma2(pack_u32x2(cur[i], cur[i + 1]), sl2x2, nbx2), a0, a1);
                         const float p0 = ex2(a0), p1 = ex2(a1);
-#ifdef TKV_ATTN_PTRUNC
+#ifdef TKV_ATTN_PTRUNC  // measured slower (DESIGN §8 "Measured and not kept"); kept as a build knob
                         // bf16 P by truncation (one PRMT per pair on the ALU instead of an F2FP), and
                         // the row sum over the same truncated values so O / l stays consistent
                         const uint32_t b0 = __float_as_uint(p0) & 0xffff0000u, b1 = __float_as_uint(p1) & 0xffff0000u;
