@@ -116,7 +116,10 @@ void Model::alloc_weights(cudaStream_t s) {
     const ModelCfg& c = cfg_;
     const long h = c.hidden(), kvd = c.kv_dim(), f = c.ffn, qd = long(c.num_heads) * c.head_dim;
     const size_t es = dtype_size(c.dtype);
+    size_t next = 0;
+    const bool refill = !allocs_.empty();  // reseed(): same buffers, new counter-hash values
     auto alloc = [&](long elems) {
+        if (refill) return allocs_[next++];
         void* p = nullptr;
         TKV_CUDA_CHECK(cudaMalloc(&p, size_t(elems) * es));
         allocs_.push_back(p);
@@ -166,6 +169,12 @@ void Model::alloc_weights(cudaStream_t s) {
     TKV_CUDA_CHECK(cudaMemsetAsync(head_, 0, size_t(vp * h) * es, s));
     launch_fill_matrix(head_, c.dtype, c.vocab, h, 0, c.seed, kHead * 131, sh, 0, 0, s);
     TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void Model::reseed(uint64_t seed, cudaStream_t s) {
+    if (seed == cfg_.seed) return;
+    cfg_.seed = seed;
+    alloc_weights(s);
 }
 
 void Model::ensure_ws(int M, cudaStream_t s) {

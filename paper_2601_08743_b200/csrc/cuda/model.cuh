@@ -123,6 +123,9 @@ class Model {
     Model(const ModelCfg& cfg, cudaStream_t s);
     ~Model();
     const ModelCfg& cfg() const { return cfg_; }
+    // regenerate every weight for another counter-hash seed in the existing buffers (the drop-in
+    // API's tests build one model per seed; a new Model would pin another staging ring each time)
+    void reseed(uint64_t seed, cudaStream_t s);
     void forward(const FwdArgs& a, cudaStream_t s);
     RopeTables& rope() { return rope_; }
     StagingRing& ring() { return ring_; }

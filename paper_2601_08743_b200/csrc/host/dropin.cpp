@@ -23,6 +23,7 @@ namespace {
 struct Slot {
     std::unique_ptr<tkv::Model> model;
     cudaStream_t stream = nullptr;
+    std::mutex mu;  // held for a whole call: reseed + compute (the API's functions are callable from any thread)
 };
 
 std::mutex g_mu;
@@ -31,8 +32,9 @@ std::map<std::tuple<int, int, int, int, int, int, int, double, std::uint64_t, in
 Slot& model_for(const ModelConfig& cfg, int precision) {
     int dev = 0;
     TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    // one device model per shape; a different weight seed regenerates the weights in place
     const auto key = std::make_tuple(dev, precision, cfg.num_layers, cfg.num_heads, cfg.kv_heads(), cfg.head_dim,
-                                     cfg.vocab_size, cfg.rotary_base, cfg.weight_seed, cfg.ffn_dim(), cfg.mlp, cfg.norm, 0);
+                                     cfg.vocab_size, cfg.rotary_base, std::uint64_t(0), cfg.ffn_dim(), cfg.mlp, cfg.norm, 0);
     std::lock_guard<std::mutex> lk(g_mu);
     auto& slot = g_models[key];
     if (!slot) {
@@ -59,6 +61,8 @@ Slot& model_for(const ModelConfig& cfg, int precision) {
 
 void forward(const Forward& f) {
     Slot& s = model_for(*f.cfg, f.precision);
+    std::lock_guard<std::mutex> use(s.mu);
+    s.model->reseed(f.cfg->weight_seed, s.stream);
     std::vector<int32_t> groups;
     if (f.groups) groups.assign(f.groups, f.groups + f.n);
     tkv::HostFwd h;
@@ -96,6 +100,7 @@ void gather_f32(const ModelConfig& cfg, const std::vector<const TableKV<float>*>
     }
     if (total == 0) return;
     Slot& s = model_for(cfg, 0);
+    std::lock_guard<std::mutex> use(s.mu);  // the gather only uses the model's rope tables (seed-free)
     tkv::Arena arena;
     tkv::PagePool pool(P, int(pages));
     std::vector<tkv::GatherSeg> segs;
