@@ -168,6 +168,23 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+// 2^x for two lanes on the FMA pipe (x >= -127): x = j + f with j = rint(x) from the 1.5*2^23
+// magic add, 2^f on [-0.5, 0.5] by a degree-3 polynomial (rel. error < 1e-3, below bf16 P's
+// rounding), exponent j added to the result's bits
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
+    const uint64_t magic = pack_f32x2(12582912.f, 12582912.f), nmagic = pack_f32x2(-12582912.f, -12582912.f);
+    const uint64_t t = fadd2(x, magic);
+    const uint64_t j = fadd2(t, nmagic);
+    uint64_t f;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(j));
+    uint64_t p = ffma2(f, pack_f32x2(0.0555041f, 0.0555041f), pack_f32x2(0.2402265f, 0.2402265f));
+    p = ffma2(p, f, pack_f32x2(0.6931472f, 0.6931472f));
+    p = ffma2(p, f, pack_f32x2(1.f, 1.f));
+    uint32_t plo, phi, tlo, thi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(plo), "=r"(phi) : "l"(p));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(t));
+    return pack_u32x2(plo + (tlo << 23), phi + (thi << 23));
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -633,8 +650,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
                         float a0, a1;
-                        unpack_f32x2(ffma2(pack_u32x2(cur[i], cur[i + 1]), sl2x2, nbx2), a0, a1);
-                        const float p0 = ex2(a0), p1 = ex2(a1);
+                        const uint64_t ax2 = ffma2(pack_u32x2(cur[i], cur[i + 1]), sl2x2, nbx2);
+                        unpack_f32x2(ax2, a0, a1);
+                        float p0, p1;
+#ifdef TKV_ATTN_EXP_EMU  // measured slower, build knob only
+                        if (i >= 32 - 2 * TKV_ATTN_EXP_EMU) {  // the chunk's last pairs on the FMA pipe
+                            unpack_f32x2(ex2_poly2(pack_f32x2(fmaxf(a0, -127.f), fmaxf(a1, -127.f))), p0, p1);
+                        } else
+#endif
+                        {
+                            p0 = ex2(a0);
+                            p1 = ex2(a1);
+                        }
 #ifdef TKV_ATTN_PTRUNC  // measured slower (DESIGN §8 "Measured and not kept"); kept as a build knob
                         // bf16 P by truncation (one PRMT per pair on the ALU instead of an F2FP), and
                         // the row sum over the same truncated values so O / l stays consistent

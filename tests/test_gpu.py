@@ -440,3 +440,40 @@ def test_executor_edge_cases():
     tiny.close()
     s.close()
     m.close()
+
+
+_PAGED_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+from paper_2601_08743_b200 import native as N
+from golden_util import demo_path, load
+kw = dict(num_layers=2, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=330, ffn_dim=512, mlp='swiglu', norm='rms')
+m = N.Model(dtype='bf16', **kw)
+s = N.Store(m, page_bytes=64 << 10, n_pages=2048)
+s.precompute(N.Engine(demo_path('demo_schema.json')))
+g = load('demo64')['result']
+qs = [(q['assembly_order'], q['remainder']) for q in g['queries'][:32]]
+res = s.serve(qs, capacity=6, b_c=8, b_m=2, want_logits=True)
+np.save(sys.argv[2], np.asarray(res['logits'], np.float32))
+s.close(); m.close()
+"""
+
+
+@pytest.mark.parametrize("variant", [{"TKV_PAGED_V": "0"}, {"TKV_K_HEAD_MAJOR": "0"}])
+def test_paged_v_and_head_major_k_bit_identical_to_slab(tmp_path, variant):
+    """Paged V (the attention reads V straight from the pool pages) and the head-major K slab move
+    the same bytes to the same smem tiles as the gathered row-major slab: the served logits must be
+    bit-identical, not merely within tolerance."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, env_over in enumerate([{}, variant]):
+        out = str(tmp_path / ("logits%d.npy" % i))
+        env = dict(os.environ, **env_over)
+        p = subprocess.run([sys.executable, "-c", _PAGED_SCRIPT, root, out], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(np.load(out))
+    assert outs[0].shape == outs[1].shape and np.isfinite(outs[0]).all()
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
