@@ -168,6 +168,7 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+#ifdef TKV_ATTN_EXP_EMU
 // 2^x for two lanes on the FMA pipe (x >= -127): x = j + f with j = rint(x) from the 1.5*2^23
 // magic add, 2^f on [-0.5, 0.5] by a degree-3 polynomial (rel. error < 1e-3, below bf16 P's
 // rounding), exponent j added to the result's bits
@@ -185,6 +186,7 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
     asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(t));
     return pack_u32x2(plo + (tlo << 23), phi + (thi << 23));
 }
+#endif
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
