@@ -70,10 +70,27 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int rows, int vo
     const float* r = logits + long(row) * ld;
     float best = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-        const float v = r[i];
+    auto take = [&](float v, int i) {
         if (v > best || (v == best && i < bi)) best = v, bi = i;
+    };
+    int i0 = 0;
+    if ((reinterpret_cast<uintptr_t>(r) & 15) == 0) {  // 16-byte loads, two in flight per thread
+        const int n4 = vocab >> 2;
+        const float4* r4 = reinterpret_cast<const float4*>(r);
+        int j = threadIdx.x;
+        for (; j + int(blockDim.x) < n4; j += 2 * blockDim.x) {
+            const float4 a = __ldg(r4 + j), b = __ldg(r4 + j + blockDim.x);
+            take(a.x, 4 * j), take(a.y, 4 * j + 1), take(a.z, 4 * j + 2), take(a.w, 4 * j + 3);
+            const int k = 4 * (j + blockDim.x);
+            take(b.x, k), take(b.y, k + 1), take(b.z, k + 2), take(b.w, k + 3);
+        }
+        for (; j < n4; j += blockDim.x) {
+            const float4 a = __ldg(r4 + j);
+            take(a.x, 4 * j), take(a.y, 4 * j + 1), take(a.z, 4 * j + 2), take(a.w, 4 * j + 3);
+        }
+        i0 = n4 << 2;
     }
+    for (int i = i0 + threadIdx.x; i < vocab; i += blockDim.x) take(r[i], i);
     __shared__ float sv[32];
     __shared__ int si[32];
     for (int o = 16; o; o >>= 1) {
@@ -115,7 +132,7 @@ void norm_bf16(const float* x, const int32_t* rows_idx, int rows, int hidden, vo
 
 void argmax_rows(const float* logits, int rows, int vocab, long ld, int32_t* out_idx, float* out_val, cudaStream_t s) {
     if (rows == 0) return;
-    argmax_kernel<<<rows, 256, 0, s>>>(logits, rows, vocab, ld, out_idx, out_val);
+    argmax_kernel<<<rows, 1024, 0, s>>>(logits, rows, vocab, ld, out_idx, out_val);
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 
