@@ -355,7 +355,8 @@ def main():
     # ---- e2e: prompt text in, first tokens out, through the C ABI (wall clock)
     # the user path: the rank's prompts in arrival order; serve_text reranks them itself
     e2e_texts = [entries[i][1] for i in sorted(my_slice(global_order()))]
-    e2e_opts = N.serve_options(rerank_on=1, capacity=args.capacity, policy=args.policy, b_c=args.b_c, b_m=args.b_m)
+    e2e_opts = N.serve_options(rerank_on=1, capacity=args.capacity, policy=args.policy, b_c=args.b_c, b_m=args.b_m,
+                               time_kernels=int(os.environ.get("TKV_E2E_TIMED", "0")))
     for _ in range(args.warmup):
         store.serve_text(eng, e2e_texts, options=e2e_opts)
     barrier()

@@ -1,5 +1,6 @@
 // Pinned host arena + paged HBM pool (see runtime.cuh).
 #include <algorithm>
+#include <functional>
 #include <cstring>
 
 #include "common.cuh"
@@ -69,7 +70,12 @@ PagePool::~PagePool() {
 
 void PagePool::reclaim() {
     while (!deferred_.empty() && cudaEventQuery(deferred_.front().ev) == cudaSuccess) {
-        for (int32_t p : deferred_.front().pages) free_.push_back(p);
+        // pushed highest id first: alloc() pops from the back, so a freed run comes back out in
+        // ascending order and a table's copy stays one contiguous run (LIFO order would hand out
+        // every other batch descending, one copy per page)
+        std::vector<int32_t>& pg = deferred_.front().pages;
+        std::sort(pg.begin(), pg.end(), std::greater<int32_t>());
+        for (int32_t p : pg) free_.push_back(p);
         cudaEventDestroy(deferred_.front().ev);
         deferred_.pop_front();
     }

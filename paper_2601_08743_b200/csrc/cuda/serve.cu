@@ -375,8 +375,17 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     DType in_dt_s = DType::bf16;
     std::vector<std::pair<int, std::vector<int32_t>>> dropped;  // evicted in the group: recycle after its compute
 
+    // The host runs at most `host_lead` windows ahead of the GPU: without a bound it queues every
+    // window's loads at once, and a window's demand copies then wait behind the prefetch backlog
+    // of later windows on the copy engines (TKV_HOST_LEAD=0: unbounded)
+    static const int host_lead = [] {
+        const char* e = std::getenv("TKV_HOST_LEAD");
+        return e ? std::atoi(e) : 2;
+    }();
     hp_tick(hp_plan);
     for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
+        if (host_lead > 0 && wi >= size_t(host_lead) && win_end[wi - host_lead])
+            TKV_CUDA_CHECK(cudaEventSynchronize(win_end[wi - host_lead]));
         const auto& w = plan.windows[wi];
         const auto& wt = tr.windows[wi];
         cur_window = wi;
