@@ -2,11 +2,13 @@
 """TableCache B200 online-path benchmark (BASELINE.json metric: p50 TTFT and prefill queries/s vs
 no-cache prefill; KV load GB/s vs PCIe).
 
-Workload (default, BASELINE.json configs[1] with the configs[2] model): Spider-like synthetic
-corpus, 40 databases / 200 tables, Zipf popularity, 1000 queries per GPU; Llama-3-8B-shaped
-decoder (32 layers, 32 q / 8 kv heads x 128, SwiGLU 14336, RMSNorm, vocab 128256), random
-(counter-hash) weights, bf16; table KV precomputed offline on the GPU into a pinned host arena;
-LRU fast tier of C = 32 tables over a paged HBM pool; rerank on; b_c = 100, b_m = 10.
+Workload (default `--config c4`, the largest single-GPU configuration of BASELINE.json: configs[2]
+prefixes with configs[3]'s capacity pressure): 16 databases / 256 tables of 256-512 tokens,
+Zipf popularity, 500 queries per GPU with 8-16 tables each (~4.7k-token cached prefixes) and
+32-128 suffix tokens; Llama-3-8B-shaped decoder (32 layers, 32 q / 8 kv heads x 128, SwiGLU
+14336, RMSNorm, vocab 128256), random (counter-hash) weights, bf16; table KV precomputed offline
+on the GPU into a pinned host arena; LRU fast tier of C = 32 tables over a paged HBM pool (every
+window evicts); rerank on; b_c = 100, b_m = 10. `--config c1|c2|c3|c5` selects the others.
 
 One step = one cold-cache batch through the whole online path: global rerank, schedule,
 canonical cache trace, H2D page copies of every miss/prefetch from the pinned arena, prefix
@@ -14,7 +16,8 @@ gather+RoPE and the batched suffix prefill with the first-token head per window.
 `value` = queries/s from CUDA-event makespans (max over ranks); `e2e` = the same batch through
 the C ABI from prompt TEXT (host analysis + D2H of first tokens) by wall clock.
 Multi-GPU (torchrun): one process per GPU, the globally reranked order is cut into contiguous
-slices (weak scaling: 1000 queries per GPU), no collective on the data path.
+slices (weak scaling: the per-GPU query count is fixed), no collective on the data path.
+`--impl reference`: the unchanged reference library (oracle/_ref) on the host cores, same metric.
 """
 import argparse
 import json
@@ -92,54 +95,113 @@ def build_workload(cfg_name, n_queries_total):
     from paper_2601_08743_b200 import workloads as W
     if cfg_name == "c1":  # the reference default: the 12-table demo schema, gen_demo queries
         return W.demo_schema(), W.demo_workload(n_queries_total)
-    spec = W.CONFIGS[cfg_name]
+    spec = W.CONFIGS["c3" if cfg_name == "c4" else cfg_name]  # c4 = c3 prefixes + capacity pressure
     spec = W.SpiderSpec(**{**spec.__dict__, "n_queries": n_queries_total})
     tables, entries, _ = W.spider_like(spec)
     return tables, entries
 
 
+METRIC = "p50 TTFT and prefill queries/sec vs no-cache prefill; KV load GB/s vs PCIe"  # BASELINE.json metric, both arms
+
+
+def ref_serve_sample(tables, entries, threads):
+    """The UNCHANGED reference library's cached serving path (oracle/_ref/ref_bench serve) on
+    this host: the first `threads` prompts of the workload, one per core, each through the
+    reference's own analyze_query + assembly_order + MemorySlowTier loads + assemble +
+    query_attend of ONE layer at the served width (hidden 4096, 32 heads x 128; reference MHA /
+    LayerNorm / SiLU-4h arithmetic, 12 h^2 MACs per token-layer vs the served GQA/SwiGLU 13 h^2).
+    The per-layer part is extrapolated x32 layers; analysis is not. Nothing here loads libtkv.so."""
+    import tempfile
+    from paper_2601_08743_b200 import workloads as W  # pure Python, no native code
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    L = LLAMA8B["num_layers"]
+    with tempfile.TemporaryDirectory() as d:
+        sp, wp = W.write_corpus(d, tables, entries[:threads])
+        out = subprocess.run([exe, "serve", sp, wp, str(threads), "32", "128", str(threads)], capture_output=True,
+                             text=True, check=True)
+    r = json.loads(out.stdout)
+    per_q = [a + L * l for a, l in zip(r["analysis_s"], r["layer_s"])]  # extrapolated service time per query
+    qps = threads / statistics.mean(per_q)  # `threads` cores serving queries back to back
+    return {"qps": qps, "wave_wall_s": r["wall_s"], "per_query_s": per_q, "raw": r,
+            "sample": "first %d prompts of the workload, one per core: reference analyze_query + assembly_order + "
+                      "loads + assemble + query_attend of 1 layer at hidden 4096 (MHA/LN/SiLU-4h; 12h^2 MACs per "
+                      "token-layer vs 13h^2 served), layer part x%d (extrapolated); mean prefix %.0f / suffix %.0f "
+                      "tokens" % (threads, L, statistics.mean(r["nctx"]), statistics.mean(r["nq"]))}
+
+
+def cpu_info():
+    import multiprocessing
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return multiprocessing.cpu_count(), model
+
+
 def reference_arm(args, rank, world):
-    """--impl reference: the reference's own CPU path (oracle/_ref/ref_bench, the unchanged
-    reference library) on this host's cores, same metric/unit, bounded sample per step."""
+    """--impl reference: the reference's own CPU path (the unchanged library, oracle/_ref) on this
+    host's cores for the same workload, metric and unit; rank 0 only. No libtkv.so is loaded.
+
+    c1: ref_bench demo (assemble + query_attend of every demo query, measured in full) once per
+    step. c2-c5: one bounded wave (one query per core, see ref_serve_sample) — a full query at
+    hidden 4096 costs the reference minutes per core, so the timed region is that single wave and
+    ms_per_step = wave wall / steps; the x32-layer extrapolation is in its own keys."""
     if rank != 0:
         return
-    import multiprocessing
+    cores, cpu_model = cpu_info()
+    tables, entries = build_workload(args.config, args.queries)
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
-    threads = multiprocessing.cpu_count()
-    tables, entries = build_workload(args.config, 1000)
-    from paper_2601_08743_b200 import native as N
-    from paper_2601_08743_b200 import workloads as W
-    eng = N.Engine(corpus_json=W.dump_schema_corpus(tables))
-    samples = []
-    for _, text in entries[:threads]:
-        a = eng.analyze(text)
-        nctx = sum(len(eng.info["table_tokens"][t]) for t in a["assembly_order"])
-        samples.append("%d:%d" % (nctx, len(a["remainder"])))
     if not os.path.exists(exe):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
         return
-    L = LLAMA8B["num_layers"]
-    per_q = []
-    walls = []
-    for step in range(args.warmup + args.steps):
-        out = subprocess.run([exe, "wide", "32", "128", str(threads), "--cached-only"] + samples, capture_output=True,
-                             text=True, check=True)
-        r = json.loads(out.stdout)
-        if step >= args.warmup:
-            per_q += [c * L for c in r["cached_s"]]
-            walls.append(r["cached_wall_s"] * L)
-    qps = len(samples) * len(walls) / sum(walls)
-    line = {"metric": "prefill queries/sec (cached path)", "value": qps, "unit": "queries/s", "impl": "reference",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "ms_per_step": sum(walls) / len(walls) * 1e3, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "c2 Spider-like 40 DBs/200 tables, Zipf, Llama-3-8B-shaped widths",
-                       "sample": "%d queries x 1 layer at hidden 4096 (reference MHA/LN/SiLU arch), x%d layers" % (len(samples), L)},
-            "p50_ttft_ms": pct(per_q, 0.5) * 1e3, "p99_ttft_ms": pct(per_q, 0.99) * 1e3,
-            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                             "sample": "%d queries of the c2 workload, query_attend of 1 layer at hidden 4096 "
-                                       "scaled x%d layers (extrapolated)" % (len(samples), L)},
-            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    base = {"metric": METRIC, "unit": "queries/s", "impl": "reference", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "data": "synthetic", "cpu": {"cores": cores, "model": cpu_model}}
+    if args.config == "c1":
+        walls, last = [], None
+        for step in range(args.warmup + args.steps):
+            last = cpu_baseline_demo(tables, entries, cores)
+            if step >= args.warmup:
+                walls.append(len(entries) / last["value"])
+        qps = len(entries) * len(walls) / sum(walls)
+        line = dict(base, value=qps, ms_per_step=sum(walls) / len(walls) * 1e3, dtype="f32",
+                    config={"workload": workload_name(args, len(tables), len(entries))},
+                    p50_ttft_ms=last["p50_query_ms"], p99_ttft_ms=last["p99_query_ms"],
+                    cpu_baseline=dict(last, value=qps))
+    else:
+        s = ref_serve_sample(tables, entries, cores)
+        wall = s["wave_wall_s"]
+        line = dict(base, value=s["qps"], ms_per_step=wall / args.steps * 1e3, dtype="f32",
+                    config={"workload": workload_name(args, len(tables), len(entries))},
+                    timed_region="one wave of %d queries (one per core) x 1 layer, %.1f s; ms_per_step = wave wall / "
+                                 "steps" % (cores, wall),
+                    extrapolated_ms_per_step=wall * LLAMA8B["num_layers"] / args.steps * 1e3,
+                    p50_query_latency_ms_extrapolated=pct(s["per_query_s"], 0.5) * 1e3,
+                    p99_query_latency_ms_extrapolated=pct(s["per_query_s"], 0.99) * 1e3,
+                    cpu_baseline={"value": s["qps"], "unit": "queries/s", "cores": cores, "kind": "reference",
+                                  "sample": s["sample"]})
+    line["e2e"] = {"value": line["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line))
+
+
+def workload_name(args, n_tables, n_queries):
+    from paper_2601_08743_b200 import workloads as W
+    if args.config == "c1":
+        return ("c1 reference default: 12-table demo schema, %d gen_demo queries, the reference model (2 layers, "
+                "4 heads x 16, LayerNorm, SiLU FFN) in f32 with the reference arithmetic" % n_queries)
+    spec = W.CONFIGS["c3" if args.config == "c4" else args.config]
+    label = {"c2": "c2 Spider-like", "c3": "c3 ~4k-token prefixes (C >= working set)",
+             "c4": "c4 = c3 prefixes + capacity pressure (evictions every window)",
+             "c5": "c5 BIRD-like wide schemas"}[args.config]
+    return ("%s: %d DBs / %d tables, Zipf(1.1), %d queries per GPU; Llama-3-8B-shaped (%d layers, 32q/8kv x128, "
+            "SwiGLU 14336, RMSNorm, vocab 128256), random weights" % (label, spec.n_db, n_tables, n_queries,
+                                                                     args.layers))
 
 
 def cpu_baseline_demo(tables, entries, threads):
@@ -161,48 +223,27 @@ def cpu_baseline_demo(tables, entries, threads):
             "p50_query_ms": r["cached_p50_ms"], "p99_query_ms": r["cached_p99_ms"]}
 
 
-def cpu_baseline_sample(eng, entries, n=4):
-    """Bounded CPU baseline on this host (rank 0, N=1): the unchanged reference library timing one
-    layer of query_attend at hidden 4096 for n queries in parallel, extrapolated to 32 layers."""
-    import multiprocessing
-    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
-    if not os.path.exists(exe):
-        return None
-    threads = min(multiprocessing.cpu_count(), max(1, n))
-    samples = []
-    for _, text in entries[:threads]:
-        a = eng.analyze(text)
-        nctx = sum(len(eng.info["table_tokens"][t]) for t in a["assembly_order"])
-        samples.append("%d:%d" % (nctx, len(a["remainder"])))
-    out = subprocess.run([exe, "wide", "32", "128", str(threads), "--cached-only"] + samples, capture_output=True, text=True,
-                         check=True)
-    r = json.loads(out.stdout)
-    L = LLAMA8B["num_layers"]
-    qps = len(samples) / (r["cached_wall_s"] * L)
-    return {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-            "sample": "%d c2 queries, reference query_attend of 1 layer at hidden 4096 (MHA/LN/SiLU), x%d layers, "
-                      "%d threads (extrapolated)" % (len(samples), L, threads),
-            "p50_query_ms": pct(r["cached_s"], 0.5) * L * 1e3}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"],
-                    help="c1 = BASELINE configs[0]: reference default (tiny model, f32 reference arithmetic, demo)")
-    ap.add_argument("--queries", type=int, default=1000, help="queries per GPU")
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE configs: c1 = reference default (tiny model, f32 reference arithmetic, demo); "
+                         "c2 Spider-like; c3 ~4k-token prefixes; c4 = c3 with capacity pressure (default: the "
+                         "largest single-GPU config); c5 BIRD-like <=16k prefixes")
+    ap.add_argument("--queries", type=int, default=None, help="queries per GPU (c2: 1000, c3/c4: 500, c5: 1250)")
     ap.add_argument("--layers", type=int, default=LLAMA8B["num_layers"])
-    ap.add_argument("--capacity", type=int, default=None, help="cache entries (default 32; c1: 6)")
+    ap.add_argument("--capacity", type=int, default=None, help="cache entries (default 32; c1: 6, c3: 256, c5: 64)")
     ap.add_argument("--policy", default="lru", choices=["lru", "fifo", "lfu"])
     ap.add_argument("--pool-pages", type=int, default=12288, help="2 MiB HBM pages in the fast-tier pool")
     ap.add_argument("--b_c", type=int, default=None, help="default 100 (c1: 1)")
     ap.add_argument("--b_m", type=int, default=None, help="default 10 (c1: 1)")
     ap.add_argument("--copy-engine", type=int, default=0, help="0: DMA copy engines, 1: SM 16-byte copy kernel")
     ap.add_argument("--sm-copy-ctas", type=int, default=16)
-    ap.add_argument("--nocache-queries", type=int, default=300, help="queries in the no-cache comparison")
+    ap.add_argument("--nocache-queries", type=int, default=None,
+                    help="queries in the no-cache comparison (c2: 300, c3/c4: 100, c5: 50)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--peer-fetch", type=int, default=None,
                     help="NVLink peer KV fetch between ranks (default: on when N > 1)")
@@ -210,14 +251,18 @@ def main():
 
     c1 = args.config == "c1"
     if args.capacity is None:
-        args.capacity = 6 if c1 else 32
+        args.capacity = {"c1": 6, "c3": 256, "c5": 64}.get(args.config, 32)
+    if args.queries is None:
+        args.queries = {"c1": 64, "c2": 1000, "c5": 1250}.get(args.config, 500)
+    if args.nocache_queries is None:
+        args.nocache_queries = {"c1": 64, "c2": 300, "c5": 50}.get(args.config, 100)
     if args.b_c is None:
         args.b_c = 1 if c1 else 100
     if args.b_m is None:
         args.b_m = 1 if c1 else 10
     if c1:
-        args.queries = min(args.queries, 64) if args.queries != 1000 else 64
-        args.nocache_queries = min(args.nocache_queries, args.queries)
+        args.queries = min(args.queries, 64)
+    args.nocache_queries = min(args.nocache_queries, args.queries)
     rank, world, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, rank, world)
@@ -387,24 +432,25 @@ def main():
     achieved_tf = gemm_fl / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
+        cores, cpu_model = cpu_info()
         try:
-            import multiprocessing
-            cpu = (cpu_baseline_demo(tables, entries, min(8, multiprocessing.cpu_count())) if c1
-                   else cpu_baseline_sample(eng, entries, n=8))
+            if c1:
+                cpu = cpu_baseline_demo(tables, entries, cores)
+            else:
+                smp = ref_serve_sample(tables, entries, cores)
+                cpu = {"value": smp["qps"], "unit": "queries/s", "cores": cores, "kind": "reference",
+                       "sample": smp["sample"], "wave_wall_s": smp["wave_wall_s"],
+                       "p50_query_latency_ms_extrapolated": pct(smp["per_query_s"], 0.5) * 1e3}
+            cpu["cpu_model"] = cpu_model
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unavailable": str(e)}
     nc_p50, c_p50 = (pct(nc["ttft_ms"], 0.5), pct(cached_sub["ttft_ms"], 0.5)) if nc_n else (None, None)
     line = {
-        "metric": "prefill queries/sec (cached path); p50/p99 TTFT vs no-cache prefill; KV load GB/s vs PCIe",
+        "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if c1 else "bf16", "data": "synthetic",
-        "config": {"workload": ("c1 reference default: 12-table demo schema, %d gen_demo queries, the reference model "
-                                "(2 layers, 4 heads x 16, LayerNorm, SiLU FFN) in f32 with the reference arithmetic"
-                                % n_local) if c1 else
-                               ("%s Spider-like: %d DBs / %d tables, Zipf(1.1), %d queries per GPU; Llama-3-8B-shaped "
-                                "(%d layers, 32q/8kv x128, SwiGLU 14336, RMSNorm, vocab 128256), random weights"
-                                % (args.config, W.CONFIGS[args.config].n_db, len(tables), n_local, args.layers)),
+        "config": {"workload": workload_name(args, len(tables), n_local),
                    "cache": "%s C=%d tables, b_c=%d, b_m=%d, rerank on, %s HBM pages"
                             % (args.policy.upper(), args.capacity, args.b_c, args.b_m, "64 KiB" if c1 else "2 MiB"),
                    "parallelism": "dp%d (request slices of the global rerank)" % world,

@@ -14,6 +14,16 @@
 //       ONE layer of the reference architecture at the given width (MHA, LN, SiLU 4h),
 //       per sample: query_attend of nq tokens over an nctx-token assembled context,
 //       and the no-cache prefill of nctx+nq tokens. The caller scales by layer count.
+//   ref_bench serve <schema.json> <workload.jsonl> <threads> <heads> <head_dim> <n_queries>
+//       the reference's cached serving path on the bench workload itself: per query, the
+//       reference's own prompt analysis (analyze_query + assembly_order, engine.cpp:133-172),
+//       MemorySlowTier loads of the matched tables' KV, assemble (attention.hpp:300-362) and
+//       query_attend (:368-414) -- ONE layer of the reference architecture at the given width
+//       (MHA, LayerNorm, SiLU 4h; the reference cannot express GQA/SwiGLU/RMSNorm). The first
+//       <n_queries> prompts (arrival order) run as one wave over <threads> cores (queries are
+//       independent, the functions are pure), after an untimed warm wave of analysis + loads +
+//       assemble (a CPU path has nothing to JIT; it pages the tables in). The caller
+//       extrapolates the per-layer part by the served model's layer count and says so.
 
 #include <algorithm>
 #include <atomic>
@@ -167,12 +177,79 @@ int cmd_wide(int argc, char** argv) {
     return 0;
 }
 
+int cmd_serve(int argc, char** argv) {
+    EngineOptions eo;
+    eo.schema_path = argv[2];
+    const double tb = now();
+    Engine e = build_engine(eo);  // tokenizer, trie, plan (the default tiny model is unused here)
+    auto workload = load_workload(argv[3]);
+    const int threads = std::stoi(argv[4]);
+    ModelConfig cfg;
+    cfg.num_layers = 1;
+    cfg.num_heads = std::stoi(argv[5]);
+    cfg.head_dim = std::stoi(argv[6]);
+    cfg.vocab_size = e.tokenizer.vocab_size();
+    cfg.weight_seed = 1;
+    const int nq = std::min<int>(std::stoi(argv[7]), int(workload.size()));
+    if (nq <= 0 || threads <= 0) throw std::runtime_error("empty sample or no threads");
+    const auto w = ModelWeights<float>::create(cfg);
+    // the slow tier: one-layer KV blocks at the wide shape for every table the sample touches
+    // (contents are irrelevant to the timing; shapes, ids and local offsets are the engine's)
+    std::vector<char> need(e.table_count(), 0);
+    for (int i = 0; i < nq; ++i)
+        for (int id : analyze_query(e, workload[i].query_id, workload[i].text).match_order) need[id] = 1;
+    auto mem = std::make_shared<MemorySlowTier>();
+    const size_t per_tok = size_t(cfg.hidden_dim());
+    for (int id = 0; id < e.table_count(); ++id) {
+        if (!need[id]) continue;
+        TableKV<float> kv;
+        kv.table_id = id;
+        kv.token_count = int(e.table_tokens[id].size());
+        kv.num_layers = 1;
+        kv.num_heads = cfg.num_heads;
+        kv.head_dim = cfg.head_dim;
+        kv.local_offset = e.local_offset[id];
+        kv.k.assign(1, std::vector<float>(size_t(kv.token_count) * per_tok, 0.01f));
+        kv.v.assign(1, std::vector<float>(size_t(kv.token_count) * per_tok, 0.02f));
+        mem->put(std::move(kv));
+    }
+    const double setup_s = now() - tb;
+    std::vector<double> analysis(nq), layer(nq), ctx(nq), qlen(nq);
+    auto wave = [&](bool attend) {
+        return run_sharded(nq, threads, [&](int i) {
+            const double t0 = now();
+            const auto q = analyze_query(e, workload[i].query_id, workload[i].text);
+            const auto order = assembly_order(e, q.match_order);
+            const double t1 = now();
+            std::vector<TableKV<float>> kvs;
+            for (int id : order) kvs.push_back(*mem->load(id));
+            const auto c = assemble<float>(cfg, e.plan, kvs, order);
+            if (attend) {
+                const auto h = query_attend<float>(cfg, w, c, q.remainder);
+                (void)h;
+            }
+            analysis[i] = t1 - t0;
+            layer[i] = now() - t1;
+            ctx[i] = c.total_tokens;
+            qlen[i] = double(q.remainder.size());
+        });
+    };
+    const double warm_s = wave(false);  // page-in: analysis + loads + assemble, no attention
+    const double wall = wave(true);
+    json out = {{"mode", "serve"}, {"layers_timed", 1}, {"heads", cfg.num_heads}, {"head_dim", cfg.head_dim},
+                {"threads", threads}, {"queries", nq}, {"setup_s", setup_s}, {"warm_s", warm_s},
+                {"wall_s", wall}, {"analysis_s", analysis}, {"layer_s", layer}, {"nctx", ctx}, {"nq", qlen}};
+    std::cout << out.dump() << "\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
         if (argc >= 6 && std::string(argv[1]) == "demo") return cmd_demo(argc, argv);
         if (argc >= 6 && std::string(argv[1]) == "wide") return cmd_wide(argc, argv);
+        if (argc >= 8 && std::string(argv[1]) == "serve") return cmd_serve(argc, argv);
         std::cerr << "usage: ref_bench demo <schema> <workload> <n> <threads> | wide <heads> <dim> <threads> <nctx:nq>...\n";
         return 2;
     } catch (const std::exception& ex) {

@@ -580,7 +580,7 @@ void tkv_store_destroy(tkv_store* s) {
     cudaSetDevice(s->model->device);
     s->server.reset();
     for (auto& kv : s->held) {
-        if (s->mesh) tkv::launch_dir_revoke(s->mesh->local_dir(), kv.first, s->model->s);
+        if (s->mesh) tkv::launch_dir_revoke(*s->mesh, kv.first, s->model->s);
         s->pool->release(kv.second, s->model->s);
     }
     cudaStreamSynchronize(s->model->s);
@@ -900,7 +900,7 @@ int tkv_store_peer_publish(tkv_store* s, int table_id) {
         const size_t P = s->pool->page_bytes();
         auto pages = s->pool->alloc(int((img->bytes + P - 1) / P));
         tkv::copy_table_to_pages(*img, *s->pool, pages, tkv::CopyEngine::dma, 16, s->model->s);
-        tkv::launch_dir_publish(m.local_dir(), table_id, page_list(pages), s->model->s);
+        tkv::launch_dir_publish(m, table_id, page_list(pages), s->model->s);
         TKV_CUDA_CHECK(cudaStreamSynchronize(s->model->s));
         s->held[table_id] = std::move(pages);
     });
@@ -912,7 +912,7 @@ int tkv_store_peer_unpublish(tkv_store* s, int table_id) {
         set_device(s->model->device);
         auto it = s->held.find(table_id);
         need(it != s->held.end(), "table not published");
-        tkv::launch_dir_revoke(mesh_of(s).local_dir(), table_id, s->model->s);
+        tkv::launch_dir_revoke(mesh_of(s), table_id, s->model->s);
         s->pool->release(it->second, s->model->s);
         TKV_CUDA_CHECK(cudaStreamSynchronize(s->model->s));
         s->held.erase(it);

@@ -251,11 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(AttnArgs a) {
 template <int D>
 void launch_d(const AttnArgs& a, int n_tiles, cudaStream_t s) {
     const int smem = AttnSmem<D>::total;
-    static bool attr = false;
-    if (!attr) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(attn_kernel<D>), smem);
     attn_kernel<D><<<n_tiles, kThreads, smem, s>>>(a);
     TKV_CUDA_CHECK(cudaGetLastError());
 }

@@ -774,11 +774,7 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
     if (n_work == 0) return;
     if (!attention_tc5_supported(a)) throw std::invalid_argument("tcgen05 attention needs head_dim 128");
     if (a.mode == 1 && !a.row_lo) throw std::invalid_argument("tcgen05 block-mask attention needs per-row group starts");
-    static bool attr = false;
-    if (!attr) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-        attr = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(attn_tc5_kernel), kSmem);
     const int kvd = a.kv_heads * D;
     const CUtensorMap mkc = a.k_hm_rows ? rows_map(a.k_ctx, a.k_hm_rows * a.kv_heads, D) : rows_map(a.k_ctx, ctx_rows, kvd);
     const CUtensorMap mvc = rows_map(a.v_ctx, ctx_rows, kvd);
@@ -791,12 +787,7 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
         TKV_CUDA_CHECK(cudaMemsetAsync(trace, 0, 16 * 1024 * 4, s));
     }
     Tc5Args args{a, work, n_work, trace};
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        TKV_CUDA_CHECK(cudaGetDevice(&dev));
-        TKV_CUDA_CHECK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int n_sm = device_sm_count();
     attn_tc5_kernel<<<std::min(n_work, n_sm), kThreads, kSmem, s>>>(mq, mkc, mvc, mko, mvo, args);
     TKV_CUDA_CHECK(cudaGetLastError());
     if (trace) {  // debug only: CTA 0's timeline of the latest launch

@@ -56,6 +56,13 @@ inline int ceil_div(long a, long b) { return int((a + b - 1) / b); }
 
 constexpr int kNumSMs = 148;
 
+// Opt `func` in to `bytes` of dynamic shared memory on the CURRENT device. The attribute is
+// per device, so the opt-in is remembered per (device, kernel) and raised only when a larger
+// size is asked for; thread-safe (the C ABI may be called from any thread, on any device).
+void ensure_smem_optin(const void* func, int bytes);
+// SM count of the current device (cached per device).
+int device_sm_count();
+
 #ifdef __CUDACC__
 // ---- bf16 ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

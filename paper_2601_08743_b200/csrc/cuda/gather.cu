@@ -315,11 +315,7 @@ void launch_gather_rope_bf16(const uint8_t* pool, size_t page_bytes, const int32
     if (gather_use_tma()) {
         // K only (paged V) needs half the staging: twice the CTAs per SM, twice the bytes in flight
         const int smem = (out_v ? 2 : 1) * kTmaRows * kvdim * 2;
-        static int attr_bytes = 0;
-        if (smem > attr_bytes) {
-            TKV_CUDA_CHECK(cudaFuncSetAttribute(gather_rope_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_bytes = smem;
-        }
+        ensure_smem_optin(reinterpret_cast<const void*>(gather_rope_tma_kernel), smem);
         gather_rope_tma_kernel<<<n_chunks, 256, smem, s>>>(pool, shift, d_page_ids, d_segs, d_chunks, L, l, kvdim, head_dim,
                                                            cos_f, sin_f, static_cast<uint8_t*>(out_k), static_cast<uint8_t*>(out_v),
                                                            k_head_major ? out_rows : 0L);

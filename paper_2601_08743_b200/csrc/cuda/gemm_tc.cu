@@ -747,11 +747,7 @@ CUtensorMap make_map_2d(const void* base, int rows, int cols, int box_rows) {
 template <int BN, int STAGES>
 void launch_tc(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     using S = Smem<BN, STAGES>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::total));
-        attr_set = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_kernel<BN, STAGES>), S::total);
     const CUtensorMap ta = make_map_2d(A, M, K, BM);
     const CUtensorMap tb = make_map_2d(B, N, K, BN);
     dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
@@ -759,25 +755,12 @@ void launch_tc(const void* A, const void* B, int M, int N, int K, const EpiParam
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        TKV_CUDA_CHECK(cudaGetDevice(&dev));
-        TKV_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return n;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int BN, int STAGES>
 void launch_persistent(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     using S = SmemP<BN, STAGES>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_persistent<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            S::total));
-        attr_set = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_persistent<BN, STAGES>), S::total);
     const CUtensorMap ta = make_map_2d(A, M, K, BM);
     const CUtensorMap tb = make_map_2d(B, N, K, BN);
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
@@ -790,11 +773,7 @@ void launch_persistent(const void* A, const void* B, int M, int N, int K, const 
 template <int STAGES>
 void launch_pair(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     using S = SmemP<256, STAGES>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_pair<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::total));
-        attr_set = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_pair<STAGES>), S::total);
     const CUtensorMap ta = make_map_2d(A, M, K, BM);
     const CUtensorMap tb = make_map_2d(B, N, K, 128);  // half of a 256-column B tile per CTA
     const int units = (((M + BM - 1) / BM + 1) / 2) * (N / 256);
@@ -806,11 +785,7 @@ void launch_pair(const void* A, const void* B, int M, int N, int K, const EpiPar
 template <int STAGES>
 void launch_2sm(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     constexpr int total = STAGES * (BM * BK * 2 + 128 * BK * 2) + (2 * STAGES + 4) * 8 + 16 + 1024;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_2sm<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, total));
-        attr_set = true;
-    }
+    ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_2sm<STAGES>), total);
     const CUtensorMap ta = make_map_2d(A, M, K, BM);
     const CUtensorMap tb = make_map_2d(B, N, K, 128);
     const int units = (((M + BM - 1) / BM + 1) / 2) * (N / 256);

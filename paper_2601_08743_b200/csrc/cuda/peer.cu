@@ -153,13 +153,16 @@ void PeerMesh::attach(const std::vector<PeerBlob>& peers) {
     }
 }
 
-void launch_dir_publish(DirEntry* dir, int t, const PageList& pages, cudaStream_t s) {
-    dir_publish_kernel<<<1, 128, 0, s>>>(dir + t, pages);
+void launch_dir_publish(const PeerMesh& m, int t, const PageList& pages, cudaStream_t s) {
+    if (t < 0 || t >= m.dir_entries()) throw std::out_of_range("peer directory: table " + std::to_string(t) + " outside it");
+    if (pages.n < 0 || pages.n > kMaxPagesPerCopy) throw std::invalid_argument("peer directory: page list too long");
+    dir_publish_kernel<<<1, 128, 0, s>>>(m.local_dir() + t, pages);
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_dir_revoke(DirEntry* dir, int t, cudaStream_t s) {
-    dir_revoke_kernel<<<1, 1, 0, s>>>(dir + t);
+void launch_dir_revoke(const PeerMesh& m, int t, cudaStream_t s) {
+    if (t < 0 || t >= m.dir_entries()) throw std::out_of_range("peer directory: table " + std::to_string(t) + " outside it");
+    dir_revoke_kernel<<<1, 1, 0, s>>>(m.local_dir() + t);
     TKV_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -79,8 +79,9 @@ class PeerMesh {
 };
 
 // owner side (stream-ordered): publish table `t` at `pages`; revoke `t`
-void launch_dir_publish(DirEntry* dir, int t, const PageList& pages, cudaStream_t s);
-void launch_dir_revoke(DirEntry* dir, int t, cudaStream_t s);
+// (bounds-checked against the mesh's directory size and kMaxPagesPerCopy)
+void launch_dir_publish(const PeerMesh& m, int t, const PageList& pages, cudaStream_t s);
+void launch_dir_revoke(const PeerMesh& m, int t, cudaStream_t s);
 // reader side: copy table `t` (`bytes`) into local `dst_pages`, each CTA from the first peer in
 // `order` holding a valid entry, else from the mapped host arena image `host_src`
 void launch_peer_fetch(const PeerView& v, const PeerOrder& order, int t, const uint8_t* host_src, size_t bytes,

@@ -1,12 +1,37 @@
 // Pinned host arena + paged HBM pool (see runtime.cuh).
 #include <algorithm>
-#include <functional>
 #include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "runtime.cuh"
 
 namespace tkv {
+
+void ensure_smem_optin(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;  // (device, kernel) -> opted-in bytes
+    int dev = 0;
+    TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = done[{dev, func}];
+    if (bytes <= have) return;
+    TKV_CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+}
+
+int device_sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> n;
+    int dev = 0;
+    TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int& c = n[dev];
+    if (!c) TKV_CUDA_CHECK(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev));
+    return c;
+}
 
 // ------------------------------------------------------------------ Arena
 Arena::~Arena() {

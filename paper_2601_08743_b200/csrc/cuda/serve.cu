@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <memory>
 #include <numeric>
 
@@ -331,6 +332,9 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         return pages;
     };
     auto page_list = [](const std::vector<int32_t>& pages) {
+        if (pages.size() > size_t(kMaxPagesPerCopy))
+            throw std::invalid_argument("peer page list: " + std::to_string(pages.size()) + " pages exceed " +
+                                        std::to_string(kMaxPagesPerCopy));
         PageList pl;
         pl.n = int(pages.size());
         for (size_t i = 0; i < pages.size(); ++i) pl.page[i] = pages[i];
@@ -351,6 +355,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     std::unordered_map<int, std::vector<int32_t>> published;
     std::vector<std::pair<int, std::vector<int32_t>>> pub_now, pub_next;
     const bool sharing = mesh_ != nullptr && managed;
+    // only tables a peer can fetch go into the directory: an id inside it and a page list that
+    // fits one DirEntry (larger tables are served from the host arena by every rank)
+    auto publishable = [&](int t, const std::vector<int32_t>& pages) {
+        return sharing && t >= 0 && t < mesh_->dir_entries() && pages.size() <= size_t(kMaxPagesPerCopy);
+    };
     if (peering) {
         TKV_CUDA_CHECK(cudaMemsetAsync(mesh_->stats(), 0, 2 * sizeof(unsigned long long), cs_));
         cudaEvent_t z = evp.get();
@@ -374,6 +383,27 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     bool in_dt_set = false;
     DType in_dt_s = DType::bf16;
     std::vector<std::pair<int, std::vector<int32_t>>> dropped;  // evicted in the group: recycle after its compute
+
+    // A throw inside the replay (pool exhausted, CUDA error, bad input) must not leak the batch's
+    // pages or leave directory entries published: drain the streams, revoke, return every page.
+    struct Unwind {
+        std::function<void()> fn;
+        bool armed = true;
+        ~Unwind() {
+            if (!armed) return;
+            try {
+                fn();
+            } catch (...) {
+            }
+        }
+    } unwind{[&] {
+        cudaDeviceSynchronize();
+        if (mesh_)
+            for (auto& kv : published) launch_dir_revoke(*mesh_, kv.first, cs_);
+        for (auto& kv : dropped) pool_.release(kv.second, cs_);
+        for (auto& kv : resident) pool_.release(kv.second, cs_);
+        cudaStreamSynchronize(cs_);
+    }};
 
     // The host runs at most `host_lead` windows ahead of the GPU: without a bound it queues every
     // window's loads at once, and a window's demand copies then wait behind the prefetch backlog
@@ -410,14 +440,14 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             if (!r.miss) continue;
             evict(r.evicted);
             resident[r.table] = load(r.table, ds_);
-            if (sharing) pub_now.push_back({r.table, resident[r.table]});
+            if (publishable(r.table, resident[r.table])) pub_now.push_back({r.table, resident[r.table]});
             R.trace.back().bytes = arena_.find(r.table)->bytes;
         }
         for (const auto& r : wt.prefetch) {
             R.trace.push_back({int(wi), 1, -1, r.table, r.evicted, true, arena_.find(r.table)->bytes});
             evict(r.evicted);
             resident[r.table] = load(r.table, ps_);
-            if (sharing) pub_next.push_back({r.table, resident[r.table]});
+            if (publishable(r.table, resident[r.table])) pub_next.push_back({r.table, resident[r.table]});
         }
         // per query: emergency reloads, then a snapshot of its tables' pages
         struct Seg {
@@ -432,7 +462,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 evict(r.evicted);
                 auto pages = load(r.table, ds_);
                 if (managed) {
-                    if (sharing) pub_now.push_back({r.table, pages});
+                    if (publishable(r.table, pages)) pub_now.push_back({r.table, pages});
                     resident[r.table] = std::move(pages);
                 }
                 else
@@ -478,7 +508,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         for (auto& [t, pages] : pub_now) {
             auto it = resident.find(t);
             if (it == resident.end() || it->second != pages) continue;
-            launch_dir_publish(mesh_->local_dir(), t, page_list(pages), cs_);
+            launch_dir_publish(*mesh_, t, page_list(pages), cs_);
             published[t] = pages;
         }
         pub_now.clear();
@@ -599,7 +629,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         for (auto& [t, pg] : dropped) {
             auto it = t >= 0 ? published.find(t) : published.end();
             if (it != published.end() && it->second == pg) {  // peers must drain before the pages recycle
-                launch_dir_revoke(mesh_->local_dir(), t, cs_);
+                launch_dir_revoke(*mesh_, t, cs_);
                 published.erase(it);
             }
             pool_.release(pg, cs_);
@@ -614,7 +644,8 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         group_first = wi + 1;
     }
     // the batch's cache dies with it: every still-resident table's pages go back to the pool
-    for (auto& kv : published) launch_dir_revoke(mesh_->local_dir(), kv.first, cs_);
+    unwind.armed = false;
+    for (auto& kv : published) launch_dir_revoke(*mesh_, kv.first, cs_);
     published.clear();
     for (auto& kv : resident) pool_.release(kv.second, cs_);
     resident.clear();

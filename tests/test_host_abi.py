@@ -163,6 +163,17 @@ def test_cache_goldens():
     assert ei.value.name == "CacheNotFull"
 
 
+def test_cache_unbounded_capacity():
+    """The reference cache is map-based: any size_t capacity, SIZE_MAX included, costs nothing
+    up front (slots are allocated as entries are admitted)."""
+    c = N.Cache(2**64 - 1, "lfu", [5] * 100)
+    for t in range(100):
+        assert c.get(t) == (False, -1)
+    assert c.get(7) == (True, -1)
+    cnt, res = c.state()
+    assert res == list(range(100)) and cnt[:3] == [1, 100, 0]
+
+
 def _cmp_run(mine, ref):
     assert mine["order"] == ref["order"]
     assert [[w["begin"], w["end"], w["demand"], w["prefetch"]] for w in mine["plan"]["windows"]] == \
