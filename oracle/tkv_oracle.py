@@ -950,6 +950,32 @@ def head_logits(cfg, W, last_row, storage="f32"):
     return (xn @ W.head().T)[0]
 
 
+def head_logits_rows(cfg, W, rows, storage="f32", chunk=8192):
+    """head_logits for several final rows at once, the head generated chunk by chunk (a
+    128256 x 4096 head is 4.2 GB in f64): same definition and rounding as head_logits."""
+    xn = norm_rows(np.asarray(rows, dtype=np.float64).reshape(-1, cfg.hidden), cfg)
+    if storage == "bf16":
+        xn = round_bf16(xn)
+    out = np.empty((xn.shape[0], cfg.vocab_size))
+    for r0 in range(0, cfg.vocab_size, chunk):
+        n = min(chunk, cfg.vocab_size - r0)
+        w = weight(cfg, "head", 0, cfg.vocab_size, cfg.hidden, storage, row_start=r0, row_count=n)
+        out[:, r0:r0 + n] = xn @ w.T
+    return out
+
+
+def groups_prefix_complete(plan_groups, group_of, assembly):
+    """True when every encoding group the assembly touches contributes a PREFIX of its encode
+    order (engine.cpp:83-112): then each cached table saw exactly the same predecessors at encode
+    time as in the no-cache block-masked prefill, and (RoPE being relative) the cached path equals
+    the no-cache one in exact arithmetic. Otherwise a table was encoded against group members the
+    query does not contain — the reference's by-design approximation (engine_test.cpp:264-269)."""
+    used = {}
+    for t in assembly:
+        used.setdefault(group_of[t], []).append(t)
+    return all(plan_groups[g][:len(ts)] == ts for g, ts in used.items())
+
+
 # ============================================================================ .kv format
 # table_kv.hpp:45-118
 
