@@ -245,6 +245,8 @@ def main():
     ap.add_argument("--nocache-queries", type=int, default=None,
                     help="queries in the no-cache comparison (c2: 300, c3/c4: 100, c5: 50)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="contiguous", choices=["interleave", "contiguous"],
+                    help="N>1: deal the global chain out in window-sized chunks (interleave) or contiguous slices")
     ap.add_argument("--peer-fetch", type=int, default=None,
                     help="NVLink peer KV fetch between ranks (default: on when N > 1)")
     args = ap.parse_args()
@@ -304,11 +306,23 @@ def main():
 
     from paper_2601_08743_b200 import sharding as S
 
-    def global_order():  # the global rerank chain, computed on this rank's GPU (bit-exact with the host chain)
-        return N.rerank_device([a["assembly_order"] for a in analyzed], n_bits, seed=1, device=local)
+    def global_order():
+        """The global rerank chain (bit-exact with the host chain), computed ONCE per step: rank 0
+        runs it on its GPU (distinct table sets, one thread-block cluster) and broadcasts the
+        permutation; every rank then takes its contiguous slice."""
+        if world == 1:
+            return N.rerank_device([a["assembly_order"] for a in analyzed], n_bits, seed=1, device=local)
+        t = torch.empty(len(analyzed), dtype=torch.int32, device=coll_dev)
+        if rank == 0:
+            t.copy_(torch.tensor(N.rerank_device([a["assembly_order"] for a in analyzed], n_bits, seed=1, device=local),
+                                 dtype=torch.int32))
+        torch.distributed.broadcast(t, 0)
+        return t.tolist()
+
+    chunk = args.b_c if args.shard == "interleave" else None
 
     def my_slice(order):
-        return S.rank_slice(order, rank, world)
+        return S.rank_slice(order, rank, world, chunk)
 
     # NVLink peer fetch: exchange pool/directory IPC blobs; peer slot i = the i-th other rank
     peer_status = "off"
@@ -342,7 +356,7 @@ def main():
         if peer_status == "on":  # every peer's slice: the host-side residency prediction
             for slot, r in enumerate(others):
                 store.peer_plan(slot, [(analyzed[i]["assembly_order"], len(analyzed[i]["remainder"]))
-                                       for i in S.rank_slice(order, r, world)])
+                                       for i in S.rank_slice(order, r, world, chunk)])
         return store.serve(qs, opts)
 
     def barrier():
@@ -453,7 +467,8 @@ def main():
         "config": {"workload": workload_name(args, len(tables), n_local),
                    "cache": "%s C=%d tables, b_c=%d, b_m=%d, rerank on, %s HBM pages"
                             % (args.policy.upper(), args.capacity, args.b_c, args.b_m, "64 KiB" if c1 else "2 MiB"),
-                   "parallelism": "dp%d (request slices of the global rerank)" % world,
+                   "parallelism": "dp%d (request shares of the global rerank: %s)" % (
+                       world, "window-sized chunks dealt round-robin" if chunk and world > 1 else "contiguous slices"),
                    "l2": "small model: weights and KV stay L2-resident (a latency-bound parity config)" if c1 else
                          "inputs larger than L2 (16 GB weights streamed per window)"},
         "p50_ttft_ms": pct(ttfts, 0.5), "p99_ttft_ms": pct(ttfts, 0.99),

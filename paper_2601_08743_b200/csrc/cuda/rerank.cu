@@ -1,144 +1,189 @@
 // Query reranking on the GPU: the greedy nearest-neighbour chain of
 // proj/src/rerank.cpp:55-94, bit-exact with the host version (rerank_packed, csrc/host/rerank.cpp).
 //
-// One CTA of 1024 threads runs the whole chain: the live queries' packed incidence rows stay in
-// shared memory when they fit (else they are read from L2), a bitmask marks chosen rows, and each
-// step is one XOR-popcount distance per remaining row followed by a block argmin on
-// (distance, slot) — slot = the row's index among live queries, so ties go to the lowest slot
-// exactly like the reference's strict `<` over ascending slots (rerank.cpp:82).
+// The host first reduces the batch to distinct table sets (rerank_classes: identical sets are
+// consumed back to back, so the chain over class representatives expanded class by class is the
+// reference chain). The class chain runs on ONE thread-block cluster of C CTAs (C = 1..16): each
+// CTA keeps its slice of the class rows in shared memory; per step every CTA takes the argmin of
+// (distance, slot) over its unused rows (slot = the class index, so ties go to the lowest slot
+// exactly like the reference's strict `<` over ascending slots, rerank.cpp:82), and pushes its
+// candidate's key AND row into every CTA's exchange slot through distributed shared memory; one
+// cluster barrier later every thread reduces the C candidates itself and already holds the
+// winner's row for the next step. One __syncthreads and one cluster barrier per step.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <vector>
 
 #include "common.cuh"
+#include "serve.cuh"
 #include "tablekv/rerank.hpp"
-#include "tablekv/rng.hpp"
 
 namespace tkv {
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kMaxWords = 64;  // tables up to 4096
+namespace cg = cooperative_groups;
 
-// the chosen-row bitmask, in 8-byte units so everything after it stays 8-byte aligned
-__host__ __device__ inline int used_u64(int m) { return (m + 63) / 64; }
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxWords = 64;    // tables up to 4096
+constexpr int kMaxCluster = 16;  // non-portable cluster size (opted in below)
+constexpr int kMaxRowsPerThread = 32;  // used-bits live in one register per thread
+constexpr size_t kSmemRowsCap = 200 * 1024;
+
+struct Xch {  // one CTA's candidate for one step
+    unsigned long long key;
+    uint64_t row[kMaxWords];
+};
+constexpr size_t kFixedSmem = sizeof(Xch) * 2 * kMaxCluster + 32 * 8 + kMaxWords * 8;
+
+__device__ __forceinline__ unsigned long long warp_min(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
+        v = x < v ? x : v;
+    }
+    return v;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
-    rerank_chain_kernel(const uint64_t* __restrict__ g_inc, int m, int words, int first, int in_smem, int32_t* __restrict__ order) {
-    extern __shared__ uint64_t sm[];
-    uint64_t* cur_row = sm;                                       // [words]
-    uint32_t* used = reinterpret_cast<uint32_t*>(sm + kMaxWords);  // [ceil(m/32)]
-    unsigned long long* red = reinterpret_cast<unsigned long long*>(sm + kMaxWords + used_u64(m));  // [32]
-    uint64_t* s_inc = reinterpret_cast<uint64_t*>(red + 32);      // [m][words] when in_smem
-    const uint64_t* inc = in_smem ? s_inc : g_inc;
+    rerank_cluster_kernel(const uint64_t* __restrict__ g_inc, int n, int words, int first, int per, int rows_in_smem,
+                          int32_t* __restrict__ order) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank()), C = int(cl.num_blocks());
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < 2 * used_u64(m); i += kThreads) used[i] = 0;
-    if (in_smem)
-        for (long i = tid; i < long(m) * words; i += kThreads) s_inc[i] = g_inc[i];
-    __syncthreads();
-    int cur = first;
-    if (tid == 0) {
-        order[0] = first;
-        used[first >> 5] |= 1u << (first & 31);
-    }
-    for (int step = 1; step < m; ++step) {
-        if (tid < words) cur_row[tid] = inc[long(cur) * words + tid];
-        __syncthreads();
-        // key = distance << 32 | slot: the minimum key is the lowest slot among the nearest rows
+    extern __shared__ __align__(16) uint64_t sm[];
+    Xch* xch = reinterpret_cast<Xch*>(sm);                                                 // [2][kMaxCluster]
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(xch + 2 * kMaxCluster);  // [32]
+    uint64_t* cur0 = reinterpret_cast<uint64_t*>(red + 32);                                 // [kMaxWords]
+    uint64_t* s_rows = cur0 + kMaxWords;                                                    // [per][words]
+    const int r0 = rank * per;
+    const int n_loc = max(0, min(n - r0, per));
+    const uint64_t* rows = rows_in_smem ? s_rows : g_inc + long(r0) * words;
+    if (rows_in_smem)
+        for (long i = tid; i < long(n_loc) * words; i += kThreads) s_rows[i] = g_inc[long(r0) * words + i];
+    if (tid < words) cur0[tid] = g_inc[long(first) * words + tid];
+    // used bits of this thread's rows: bit j <-> local row tid + j * kThreads
+    uint32_t used = 0;
+    if (first >= r0 && first < r0 + n_loc && (first - r0) % kThreads == tid) used |= 1u << ((first - r0) / kThreads);
+    if (rank == 0 && tid == 0) order[0] = first;
+    cl.sync();  // every CTA's exchange area exists before the first remote store
+    const uint64_t* cur = cur0;
+    for (int step = 1; step < n; ++step) {
         unsigned long long best = ~0ull;
-        for (int i = tid; i < m; i += kThreads) {
-            if (used[i >> 5] & (1u << (i & 31))) continue;
-            const uint64_t* row = inc + long(i) * words;
+        int j = 0;
+        for (int i = tid; i < n_loc; i += kThreads, ++j) {
+            if ((used >> j) & 1u) continue;
+            const uint64_t* row = rows + long(i) * words;
             uint32_t d = 0;
-            for (int w = 0; w < words; ++w) d += __popcll(row[w] ^ cur_row[w]);
-            const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | uint32_t(i);
+            for (int w = 0; w < words; ++w) d += __popcll(row[w] ^ cur[w]);
+            const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | uint32_t(r0 + i);
             best = key < best ? key : best;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-            best = other < best ? other : best;
-        }
+        best = warp_min(best);
         if (lane == 0) red[warp] = best;
         __syncthreads();
+        const int par = step & 1;
         if (warp == 0) {
-            best = red[lane];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-                best = other < best ? other : best;
-            }
-            if (lane == 0) {
-                const int pick = int(uint32_t(best));
-                order[step] = pick;
-                used[pick >> 5] |= 1u << (pick & 31);
-                red[0] = best;
+            best = warp_min(lane < kWarps ? red[lane] : ~0ull);
+            const bool has = best != ~0ull;
+            const long li = has ? long(uint32_t(best)) - r0 : 0;
+            for (int dst = 0; dst < C; ++dst) {  // this CTA's candidate -> slot [par][rank] of every CTA
+                Xch* x = cl.map_shared_rank(&xch[par * kMaxCluster + rank], dst);
+                if (lane == 0) x->key = best;
+                if (has)
+                    for (int w = lane; w < words; w += 32) x->row[w] = rows[li * words + w];
             }
         }
-        __syncthreads();
-        cur = int(uint32_t(red[0]));
+        cl.sync();
+        unsigned long long win = ~0ull;
+        int wr = 0;
+        for (int r = 0; r < C; ++r) {
+            const unsigned long long k = xch[par * kMaxCluster + r].key;
+            if (k < win) win = k, wr = r;
+        }
+        cur = xch[par * kMaxCluster + wr].row;  // read during the next step; rewritten two steps later
+        const int ls = int(uint32_t(win)) - r0;
+        if (ls >= 0 && ls < n_loc && ls % kThreads == tid) used |= 1u << (ls / kThreads);
+        if (rank == 0 && tid == 0) order[step] = int32_t(uint32_t(win));
     }
 }
 
+// per-thread device scratch, grown on demand and kept (no allocator traffic per batch)
+struct Scratch {
+    int device = -1;
+    uint64_t* inc = nullptr;
+    int32_t* order = nullptr;
+    size_t cap_inc = 0, cap_order = 0;
+};
+
 }  // namespace
+
+std::vector<size_t> rerank_chain_device(const uint64_t* rows, size_t m, size_t words, size_t first, cudaStream_t s) {
+    if (m == 0) return {};
+    if (words > size_t(kMaxWords)) throw std::invalid_argument("device rerank supports up to 4096 tables");
+    if (m > size_t(kMaxCluster) * kThreads * kMaxRowsPerThread) throw std::invalid_argument("device rerank: batch too large");
+    // smallest cluster whose slices fit shared memory with at most 4 rows per thread; beyond 16
+    // CTAs the rows stay in global memory (L2) instead
+    int C = 1;
+    auto fits = [&](int c) {
+        const size_t per = (m + size_t(c) - 1) / size_t(c);
+        return per * words * 8 <= kSmemRowsCap && per <= size_t(4 * kThreads);
+    };
+    while (C < kMaxCluster && !fits(C)) C *= 2;
+    const size_t per = (m + size_t(C) - 1) / size_t(C);
+    const bool in_smem = per * words * 8 <= kSmemRowsCap;
+    if (per > size_t(kThreads) * kMaxRowsPerThread) throw std::invalid_argument("device rerank: batch too large");
+    const size_t smem = kFixedSmem + (in_smem ? per * words * 8 : 0);
+
+    static thread_local Scratch sc;
+    int dev = 0;
+    TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    if (sc.device != dev) sc = Scratch{}, sc.device = dev;  // (a previous device's buffers are left to it)
+    if (sc.cap_inc < m * words) {
+        cudaFree(sc.inc);
+        sc.cap_inc = std::max<size_t>(m * words, 1 << 16);
+        TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.inc), sc.cap_inc * 8));
+    }
+    if (sc.cap_order < m) {
+        cudaFree(sc.order);
+        sc.cap_order = std::max<size_t>(m, 1 << 14);
+        TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.order), sc.cap_order * 4));
+    }
+    TKV_CUDA_CHECK(cudaMemcpyAsync(sc.inc, rows, m * words * 8, cudaMemcpyHostToDevice, s));
+    ensure_smem_optin(reinterpret_cast<const void*>(rerank_cluster_kernel), int(smem));
+    static thread_local int nonportable_dev = -1;
+    if (nonportable_dev != dev) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(rerank_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        nonportable_dev = dev;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(C));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TKV_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rerank_cluster_kernel, static_cast<const uint64_t*>(sc.inc), int(m), int(words),
+                                      int(first), int(per), int(in_smem), sc.order));
+    std::vector<int32_t> ord(m);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), sc.order, m * 4, cudaMemcpyDeviceToHost, s));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+    return std::vector<size_t>(ord.begin(), ord.end());
+}
 
 std::vector<size_t> rerank_device(const uint64_t* inc, size_t n, size_t words, uint64_t seed, tablekv::AnchorMode mode,
                                   cudaStream_t s) {
-    if (n == 0) throw tablekv::Error(tablekv::Errc::empty_batch, "rerank needs at least one query");
     if (words > size_t(kMaxWords)) throw std::invalid_argument("device rerank supports up to 4096 tables");
-    std::vector<size_t> live, empty;
-    for (size_t i = 0; i < n; ++i) {
-        bool any = false;
-        for (size_t w = 0; w < words && !any; ++w) any = inc[i * words + w] != 0;
-        (any ? live : empty).push_back(i);
-    }
-    std::vector<size_t> out;
-    out.reserve(n);
-    if (!live.empty()) {
-        const size_t m = live.size();
-        size_t first = 0;
-        if (mode == tablekv::AnchorMode::seeded) {  // rerank.cpp:68-71
-            tablekv::SeededRng r(seed);
-            first = size_t(r.next_below(m));
-        }
-        std::vector<uint64_t> packed(m * words);
-        for (size_t k = 0; k < m; ++k) std::copy(inc + live[k] * words, inc + (live[k] + 1) * words, packed.begin() + long(k * words));
-        // per-thread device scratch, grown on demand and kept (no allocator traffic per batch)
-        struct Scratch {
-            int device = -1;
-            uint64_t* inc = nullptr;
-            int32_t* order = nullptr;
-            size_t cap = 0;
-        };
-        static thread_local Scratch sc;
-        int dev = 0;
-        TKV_CUDA_CHECK(cudaGetDevice(&dev));
-        if (sc.device != dev || sc.cap < m * (words + 1)) {
-            if (sc.device == dev) {
-                cudaFree(sc.inc);
-                cudaFree(sc.order);
-            }
-            sc.device = dev;
-            sc.cap = std::max<size_t>(m * (words + 1), 1 << 16);
-            TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.inc), sc.cap * 8));
-            TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.order), sc.cap * 4));
-            TKV_CUDA_CHECK(cudaFuncSetAttribute(rerank_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 4096));
-        }
-        TKV_CUDA_CHECK(cudaMemcpyAsync(sc.inc, packed.data(), packed.size() * 8, cudaMemcpyHostToDevice, s));
-        const size_t base = (kMaxWords + size_t(used_u64(int(m))) + 32) * 8;
-        const size_t full = base + packed.size() * 8;
-        const bool in_smem = full <= 200 * 1024;
-        const size_t smem = in_smem ? full : base;
-        if (smem > 200 * 1024 + 4096) throw std::invalid_argument("device rerank: batch too large for one CTA's bitmask");
-        rerank_chain_kernel<<<1, kThreads, smem, s>>>(sc.inc, int(m), int(words), int(first), int(in_smem), sc.order);
-        TKV_CUDA_CHECK(cudaGetLastError());
-        std::vector<int32_t> ord(m);
-        TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), sc.order, m * 4, cudaMemcpyDeviceToHost, s));
-        TKV_CUDA_CHECK(cudaStreamSynchronize(s));
-        for (int32_t k : ord) out.push_back(live[size_t(k)]);
-    }
-    out.insert(out.end(), empty.begin(), empty.end());  // rerank.cpp:92
-    return out;
+    const tablekv::RerankClasses rc = tablekv::rerank_classes(inc, n, words, seed, mode);
+    if (rc.n_classes() == 0) return rc.empty;
+    return tablekv::expand_class_chain(rc, rerank_chain_device(rc.rows.data(), rc.n_classes(), words, rc.anchor_class, s));
 }
 
 }  // namespace tkv

@@ -225,8 +225,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             peer_live.push_back(it == peer_plans_.end() ? decltype(peer_live)::value_type{}
                                                         : residency_intervals(plan_batch(it->second.tables, it->second.suffix_len, opts, arena_)));
         }
-    // the peers whose pool should hold table t when this GPU fetches for window w (the copy runs
-    // during compute(w-1), when a peer in step is around its window w-1); -1 terminated
+    // the peers whose pool should hold table t when this GPU fetches for window w: the copy runs
+    // during compute(w-1), when a peer in step is between its windows w-1 and w, so a peer whose
+    // predicted residency overlaps [w-1, w] is tried first (each copy CTA re-checks the live
+    // directory entry and falls back to the host arena if the table is not published yet or any
+    // more); -1 terminated
     auto predict = [&](int t, int w) {
         PeerOrder o;
         for (int i = 0; i < kMaxPeers; ++i) o.p[i] = -1;
@@ -235,7 +238,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             auto it = peer_live[p].find(t);
             if (it == peer_live[p].end()) continue;
             for (const auto& iv : it->second)
-                if (iv.first <= w - 1 && iv.second >= w - 1) {
+                if (iv.first <= w && iv.second >= w - 1) {
                     o.p[k++] = int8_t(p);
                     break;
                 }

@@ -1,9 +1,16 @@
 """Request partitioning across GPUs.
 
-Every rank computes the SAME global rerank chain (deterministic: seeded anchor, strict-< ties,
-rerank.cpp:55-94) and serves a contiguous slice of it with rerank off — contiguous slices keep the
-chain's locality, so each rank's cache sees neighbouring queries. No collective touches the data
-path; each rank owns a model replica, a TieredCache trace, a page pool and an executor.
+The global rerank chain (deterministic: seeded anchor, strict-< ties, rerank.cpp:55-94) is cut
+into per-rank shares that each rank serves with rerank off; no collective touches the data path
+(each rank owns a model replica, a TieredCache trace, a page pool and an executor).
+
+* contiguous (`chunk=None`): rank r takes the r-th contiguous slice — maximal locality inside a
+  rank, but neighbouring ranks meet the same tables only at slice boundaries, at opposite ends
+  of their timelines, so NVLink peer fetch has nothing to fetch;
+* interleaved (`chunk=b_c`): the chain is dealt out in chunks of one serving window, chunk k to
+  rank k mod world. Neighbouring chunks (similar table sets) then run on different ranks at the
+  same window index, so a rank's miss usually finds the table resident in a peer's pool at that
+  moment and is copied over NVLink instead of PCIe (the peer path's routing, serve.cu).
 """
 from __future__ import annotations
 
@@ -20,6 +27,8 @@ def global_order(table_sets, n_bits, seed=1):
     return native.rerank(table_sets, n_bits, seed=seed)
 
 
-def rank_slice(order, rank, world):
+def rank_slice(order, rank, world, chunk=None):
+    if chunk:
+        return [q for k in range(rank * chunk, len(order), world * chunk) for q in order[k:k + chunk]]
     lo, hi = slice_bounds(len(order), rank, world)
     return list(order[lo:hi])

@@ -332,8 +332,9 @@ def test_bf16_serving_path_matches_per_query_forward():
 @pytest.mark.parametrize("n,n_bits,seed", [(1, 12, 1), (64, 12, 1), (600, 200, 3), (3000, 200, 7), (9000, 660, 1),
                                            (2500, 4096, 5)])
 def test_device_rerank_identical_to_reference_chain(n, n_bits, seed):
-    """rerank on the GPU (one CTA, (distance, slot) argmin) == the host chain pinned to the
-    reference's goldens (strict-< ties to the lowest slot, empty sets last, seeded anchor)."""
+    """rerank on the GPU (class chain on one thread-block cluster, (distance, slot) argmin) == the
+    host chain pinned to the reference's goldens (strict-< ties to the lowest slot, empty sets
+    last, seeded anchor); small sets from 40 tables: many duplicate sets and distance ties."""
     rng = np.random.default_rng(seed)
     sets = []
     for i in range(n):
@@ -341,6 +342,27 @@ def test_device_rerank_identical_to_reference_chain(n, n_bits, seed):
         sets.append(sorted(set(rng.integers(0, min(n_bits, 40), k).tolist())) if i % 17 else [])
     for mode in ("seeded", "fixed_first"):
         assert N.rerank_device(sets, n_bits, seed=seed, mode=mode) == N.rerank(sets, n_bits, seed=seed, mode=mode)
+
+
+@pytest.mark.parametrize("n,n_bits,per_db,seed", [(10000, 660, 60, 1), (4000, 4096, 300, 2), (20000, 660, 60, 3)])
+def test_device_rerank_distinct_sets_at_c5_scale(n, n_bits, per_db, seed):
+    """The C5 / 8-GPU global chain: 10k-20k queries of 10-50 tables drawn inside 60-table
+    databases (every set distinct, so the class reduction does not shrink it), and 4k queries over
+    4096 tables: the multi-CTA cluster chain equals the host chain; its time is printed."""
+    import time
+    rng = np.random.default_rng(seed)
+    sets = []
+    for i in range(n):
+        db = int(rng.integers(0, n_bits // per_db))
+        k = int(rng.integers(10, 51)) if per_db == 60 else int(rng.integers(2, 9))
+        sets.append(sorted((db * per_db + rng.choice(per_db, size=min(k, per_db), replace=False)).tolist()))
+    N.rerank_device(sets[:100], n_bits, seed=seed)  # warm-up (scratch, attributes)
+    t0 = time.perf_counter()
+    dev = N.rerank_device(sets, n_bits, seed=seed)
+    ms = (time.perf_counter() - t0) * 1e3
+    host = N.rerank(sets, n_bits, seed=seed)
+    assert dev == host
+    print("device rerank: %d queries x %d tables: %.1f ms" % (n, n_bits, ms))
 
 
 def test_load_dir_reference_and_bf16_images(tmp_path, f32_store):

@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import golden_inputs as GI
+import tkv_oracle as O
 from golden_util import demo_path, load
 
 N = pytest.importorskip("paper_2601_08743_b200.native")
@@ -142,6 +143,19 @@ def test_rerank_goldens_single_and_multithreaded():
     a = N.rerank(sets, 300, 7, threads=1)
     b = N.rerank(sets, 300, 7, threads=8)
     assert a == b and sorted(a) == list(range(5000))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_rerank_class_reduction_equals_row_chain(seed):
+    """rerank_packed chains distinct table sets and expands each class in ascending slot order
+    (rerank_classes): on batches full of duplicate sets, empty sets and anchors landing inside a
+    class, the order equals the oracle's row-by-row restatement of rerank.cpp:55-94."""
+    rng = np.random.default_rng(seed)
+    base = [sorted(set(rng.integers(0, 20, rng.integers(0, 4)).tolist())) for _ in range(12)]
+    sets = [base[int(rng.integers(0, len(base)))] for _ in range(300)]
+    for mode in ("seeded", "fixed_first"):
+        for s in (seed, seed + 10, seed + 20):
+            assert N.rerank(sets, 20, s, mode) == O.rerank(sets, 20, s, mode)
 
 
 def test_cache_goldens():

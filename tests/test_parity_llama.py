@@ -16,7 +16,7 @@ Oracle: tkv_oracle.encode_group -> assemble -> query_attend -> head_logits_rows 
 verify_query comparison of engine.cpp:174-205 / acceptance.cpp:112-135 on first-token logits.
 
 Tolerances (stated): encoded K/V within 2 bf16 ulps (relative 2^-7) of the oracle's bf16 values
-or 2e-2 absolute; first-token logits within LOGIT_TOL = 3e-2 absolute; argmax equal for 100% of
+or 2e-2 absolute; first-token logits within LOGIT_TOL = 1e-2 absolute; argmax equal for 100% of
 the queries whose oracle top-2 margin exceeds 2 * LOGIT_TOL (the band where a rounding-order
 difference of up to LOGIT_TOL on each logit could swap them). The in-band count and the margin
 distribution are reported (TKV_PARITY_REPORT=<path> writes them as JSON).
@@ -34,7 +34,7 @@ pytestmark = pytest.mark.gpu
 N = pytest.importorskip("paper_2601_08743_b200.native")
 from paper_2601_08743_b200 import workloads as WL  # noqa: E402
 
-LOGIT_TOL = 3e-2
+LOGIT_TOL = 1e-2  # measured max 7.5e-3 over 99 queries (profiles/r2_parity_llama2l.json)
 LLAMA2L = dict(num_layers=2, num_heads=32, num_kv_heads=8, head_dim=128, ffn_dim=14336, vocab_size=128256,
                mlp="swiglu", norm="rms")
 REPORT = {}
