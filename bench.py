@@ -193,8 +193,10 @@ def reference_arm(args, rank, world):
 def workload_name(args, n_tables, n_queries):
     from paper_2601_08743_b200 import workloads as W
     if args.config == "c1":
+        arith = ("bf16 on the tensor-core kernels" if getattr(args, "dtype", None) == "bf16" else
+                 "f32 with the reference arithmetic")
         return ("c1 reference default: 12-table demo schema, %d gen_demo queries, the reference model (2 layers, "
-                "4 heads x 16, LayerNorm, SiLU FFN) in f32 with the reference arithmetic" % n_queries)
+                "4 heads x 16, LayerNorm, SiLU FFN) in %s" % (n_queries, arith))
     spec = W.CONFIGS["c3" if args.config == "c4" else args.config]
     label = {"c2": "c2 Spider-like", "c3": "c3 ~4k-token prefixes (C >= working set)",
              "c4": "c4 = c3 prefixes + capacity pressure (evictions every window)",
@@ -245,6 +247,10 @@ def main():
     ap.add_argument("--nocache-queries", type=int, default=None,
                     help="queries in the no-cache comparison (c2: 300, c3/c4: 100, c5: 50)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", default=None, choices=["f32", "bf16"],
+                    help="c1 only: f32 = the reference arithmetic on the SIMT parity kernels (default), bf16 = the "
+                         "same reference model on the tensor-core kernels (tcgen05 GEMMs, mma.sync head_dim-16 "
+                         "attention); c2-c5 are always bf16")
     ap.add_argument("--shard", default="contiguous", choices=["interleave", "contiguous"],
                     help="N>1: deal the global chain out in window-sized chunks (interleave) or contiguous slices")
     ap.add_argument("--peer-fetch", type=int, default=None,
@@ -252,6 +258,8 @@ def main():
     args = ap.parse_args()
 
     c1 = args.config == "c1"
+    args.dtype = (args.dtype or "f32") if c1 else "bf16"
+    c1_simt = c1 and args.dtype == "f32"
     if args.capacity is None:
         args.capacity = {"c1": 6, "c3": 256, "c5": 64}.get(args.config, 32)
     if args.queries is None:
@@ -291,7 +299,7 @@ def main():
     mk = dict(LLAMA8B, num_layers=args.layers)
     t0 = time.time()
     if c1:  # the reference's own model (model.hpp defaults) in f32 with the reference arithmetic
-        model = N.Model(dtype="f32", device=local, num_layers=2, num_heads=4, head_dim=16,
+        model = N.Model(dtype=args.dtype, device=local, num_layers=2, num_heads=4, head_dim=16,
                         vocab_size=eng.info["vocab_size"])
         store = N.Store(model, page_bytes=64 << 10, n_pages=2048)
     else:
@@ -463,7 +471,7 @@ def main():
         "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if c1 else "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": workload_name(args, len(tables), n_local),
                    "cache": "%s C=%d tables, b_c=%d, b_m=%d, rerank on, %s HBM pages"
                             % (args.policy.upper(), args.capacity, args.b_c, args.b_m, "64 KiB" if c1 else "2 MiB"),
@@ -492,7 +500,7 @@ def main():
         "roofline": {"bound": "latency", "kernel": "reference-precision SIMT forward (simt.cu)", "achieved": None,
                      "peak": None, "unit": None, "frac": None, "traffic": None,
                      "note": "c1 runs the reference's f32/double arithmetic for bit-level parity; tensor-core "
-                             "rooflines are reported on c2-c5"} if c1 else
+                             "rooflines are reported on c2-c5 and on c1 --dtype bf16"} if c1_simt else
                     {"bound": "tensor", "kernel": "gemm_tc (tcgen05 QKV/O/gate-up/down/head)",
                      "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": traffic.get("dram_bytes_per_launch"),

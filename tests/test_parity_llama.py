@@ -71,12 +71,12 @@ class Setup:
     """One corpus: the oracle's engine plan (pinned to the reference), the GPU engine + store with
     the bf16 GPU precompute of every table, and the oracle's encode of the groups in use."""
 
-    def __init__(self, model, W, name, n_queries, pick, limit=None):
-        self.cfg = _cfg()
-        tables, entries = _corpus(name, n_queries)
+    def __init__(self, model, W, name, n_queries, pick, limit=None, cfg=None, corpus=None):
+        self.cfg = cfg or _cfg()
+        tables, entries = corpus or _corpus(name, n_queries)
         self.plan = O.build_engine(tables)
         self.eng = N.Engine(corpus_json=WL.dump_schema_corpus(tables))
-        self.store = N.Store(model, page_bytes=2 << 20, n_pages=1024)
+        self.store = N.Store(model, page_bytes=(2 << 20) if cfg is None else (64 << 10), n_pages=1024)
         self.store.precompute(self.eng)
         self.store.bind_engine(self.eng)  # table tokens + groups for the no-cache baseline
         self.queries = []
@@ -232,3 +232,29 @@ def test_bf16_served_first_token_matches_oracle_long_prefix(model, oracle_weight
         assert s["argmax_equal_outside_band"] == s["outside_band"], s
     finally:
         st.close()
+
+
+def test_bf16_c1_bench_config_matches_oracle():
+    """BASELINE configs[0] (the reference default) on the tensor-core kernels, exactly as
+    `bench.py --config c1 --dtype bf16` serves it: the reference model (2 layers, 4 heads x 16,
+    LayerNorm, SiLU FFN, vocab from the demo corpus) in bf16, the demo schema and its 64 gen_demo
+    prompts, bf16 GPU precompute, LRU C=6, b_c=b_m=1; every first-token logit row vs the oracle's
+    encode_group -> assemble -> query_attend -> head in bf16 storage."""
+    tables, entries = WL.demo_schema(), WL.demo_workload(64)
+    eng = N.Engine(corpus_json=WL.dump_schema_corpus(tables))
+    cfg = O.ModelConfig(vocab_size=eng.info["vocab_size"])
+    m = N.Model(dtype="bf16", num_layers=2, num_heads=4, head_dim=16, vocab_size=eng.info["vocab_size"])
+    W = O.Weights(cfg, "bf16")
+    st = Setup(m, W, "c1", 64, lambda asm, rem, plan: True, cfg=cfg, corpus=(tables, entries))
+    try:
+        res = st.store.serve(st.queries, capacity=6, policy="lru", b_c=1, b_m=1, want_logits=True)
+        last = [st.oracle_cached_logits(*st.queries[qi]) for qi in res["order"]]
+        ref = O.head_logits_rows(cfg, W, np.stack(last), "bf16")
+        rows = [_check_logits("c1", res["logits"][i], ref[i]) for i in range(len(res["order"]))]
+        s = _summarise("c1_bf16", rows)
+        assert s["queries"] == 64
+        assert s["max_abs_logit_err"] <= LOGIT_TOL, s
+        assert s["argmax_equal_outside_band"] == s["outside_band"], s
+    finally:
+        st.close()
+        m.close()
