@@ -130,6 +130,10 @@ int tkv_store_load_dir(tkv_store* s, const char* dir, const tkv_engine* e, int t
 /* offline encode of every group on the GPU (precompute_corpus, engine.cpp:83-112) into the arena;
  * out_dir (nullable) also gets <id>.kv files (f32 models: the reference format) + manifest.json */
 int tkv_store_precompute(tkv_store* s, const tkv_engine* e, const char* out_dir);
+/* stats of the last precompute into out[0..n): groups, tables, tokens, forwards, device ms (encode
+ * forwards + D2H into the arena), GEMM ms, GEMM flops, attention ms, kernel launches (the timed
+ * fields need timed_next = 1 set before that precompute: CUDA events around each launch) */
+int tkv_store_precompute_stats(const tkv_store* s, int timed_next, double* out, int n);
 /* copy a table into pool pages (one miss), read the landed bytes back (bytes-exact check) */
 int tkv_store_fetch(tkv_store* s, int table_id, int copy_engine, void* host_out, size_t bytes);
 /* assemble() on the GPU (attention.hpp:300-362): k_out/v_out [L][total][kv_dim] (dense, row stride

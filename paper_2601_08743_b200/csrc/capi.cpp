@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstring>
 #include <filesystem>
@@ -47,6 +48,9 @@ struct tkv_store {
     std::unique_ptr<tkv::Server> server;
     std::unique_ptr<tkv::PeerMesh> mesh;
     std::unordered_map<int, std::vector<int32_t>> held;  // peer_publish: table -> pages
+    // last precompute: groups, tables, tokens, forwards, device ms, gemm ms, gemm flops, attention ms, launches
+    std::array<double, 9> encode_stats{};
+    bool encode_timed = false;  // CUDA-event timing of the next precompute's GEMM / attention launches
 };
 
 namespace {
@@ -686,15 +690,26 @@ int tkv_store_bind_engine(tkv_store* s, const tkv_engine* e) {
     });
 }
 
+// Offline encode (precompute_corpus, engine.cpp:83-112; encode_group, attention.hpp:254-294) on
+// the GPU. Groups are packed into block-causal mode-1 forwards: one sequence per group at its
+// local positions 0..n-1 (encode_group's single causal block), up to TKV_ENCODE_ROWS (16384)
+// tokens per forward, groups taken largest first so each forward's attention items are alike.
+// Every row's result is independent of what else shares its forward (row-wise GEMM tiles,
+// per-sequence attention), so the images equal one forward per group. Each table's raw K and V
+// go from the forward's [L][M][kv_dim] outputs straight into its pinned arena image by one 2-D
+// copy each (no host staging); .kv / .kvb files are written from the images afterwards.
 int tkv_store_precompute(tkv_store* s, const tkv_engine* eh, const char* out_dir) {
     return guard([&] {
         need(s && eh, "null argument");
         namespace fs = std::filesystem;
         const auto& e = eh->e;
         tkv_model* m = s->model;
-        const auto& c = m->m->cfg();
+        set_device(m->device);
+        tkv::Model& model = *m->m;
+        const auto& c = model.cfg();
         const int L = c.num_layers, kvd = c.kv_dim();
         const size_t es = tkv::dtype_size(c.dtype);
+        const size_t row = size_t(kvd) * es;
         need(c.dtype != tkv::DType::f64, "precompute stores f32 or bf16 images");
         const tkv::DType img_dt = c.dtype;
         fs::path tmp;
@@ -704,41 +719,129 @@ int tkv_store_precompute(tkv_store* s, const tkv_engine* eh, const char* out_dir
             fs::remove_all(tmp, ec);
             if (!fs::create_directories(tmp)) throw tablekv::Error(tablekv::Errc::io_error, "cannot create " + tmp.string());
         }
-        for (const auto& g : e.plan.groups) {
-            std::vector<int32_t> toks;
-            for (int t : g.tables) {
+        std::vector<int> gsz(e.plan.groups.size(), 0), gorder(e.plan.groups.size());
+        for (size_t gi = 0; gi < e.plan.groups.size(); ++gi) {
+            for (int t : e.plan.groups[gi].tables) {
                 if (e.table_tokens[size_t(t)].empty())
                     throw tablekv::Error(tablekv::Errc::empty_group, "table " + std::to_string(t) + " has no tokens");
-                toks.insert(toks.end(), e.table_tokens[size_t(t)].begin(), e.table_tokens[size_t(t)].end());
+                gsz[gi] += int(e.table_tokens[size_t(t)].size());
             }
-            const int n = int(toks.size());
-            std::vector<int32_t> grp(static_cast<size_t>(n), 0), pos(static_cast<size_t>(n));
-            std::iota(pos.begin(), pos.end(), 0);
-            std::vector<uint8_t> kraw(size_t(L) * n * kvd * es), vv(kraw.size());
-            const int rc = tkv_model_forward(m, toks.data(), pos.data(), grp.data(), n, 1, nullptr, nullptr, 0, nullptr,
-                                             kraw.data(), vv.data(), nullptr, nullptr);
-            if (rc != TKV_OK) throw std::runtime_error("precompute forward failed: " + g_err);
-            for (size_t i = 0; i < g.tables.size(); ++i) {
-                const int t = g.tables[i], off = g.offsets[i], T = int(e.table_tokens[size_t(t)].size());
-                std::vector<uint8_t> img(size_t(2) * L * T * kvd * es);
-                const size_t row = size_t(kvd) * es;
-                for (int kvi = 0; kvi < 2; ++kvi)
-                    for (int l = 0; l < L; ++l)
-                        std::memcpy(img.data() + (size_t(kvi) * L + l) * T * row, (kvi ? vv : kraw).data() + (size_t(l) * n + off) * row,
-                                    size_t(T) * row);
-                if (!s->arena->find(t)) s->arena->put(t, T, L, kvd, off, img_dt, img.data());
-                if (out_dir) {
+        }
+        std::iota(gorder.begin(), gorder.end(), 0);
+        std::stable_sort(gorder.begin(), gorder.end(), [&](int x, int y) { return gsz[size_t(x)] > gsz[size_t(y)]; });
+        static const int kRows = [] {
+            const char* v = std::getenv("TKV_ENCODE_ROWS");
+            return v ? std::max(1, std::atoi(v)) : 16384;
+        }();
+        std::vector<std::vector<int>> batches;
+        for (size_t i = 0, rows = 0; i < gorder.size(); ++i) {
+            const int gs = gsz[size_t(gorder[i])];
+            if (batches.empty() || rows + size_t(gs) > size_t(kRows)) batches.emplace_back(), rows = 0;
+            batches.back().push_back(gorder[i]);
+            rows += size_t(gs);
+        }
+        int max_rows = 1;
+        for (const auto& bt : batches) {
+            int r = 0;
+            for (int gi : bt) r += gsz[size_t(gi)];
+            max_rows = std::max(max_rows, r);
+        }
+        cudaStream_t st = m->s;
+        void *dk = nullptr, *dv = nullptr;
+        TKV_CUDA_CHECK(cudaMalloc(&dk, size_t(L) * max_rows * row));
+        struct Free {
+            void*& a;
+            void*& b;
+            ~Free() {
+                if (a) cudaFree(a);
+                if (b) cudaFree(b);
+            }
+        } freer{dk, dv};
+        TKV_CUDA_CHECK(cudaMalloc(&dv, size_t(L) * max_rows * row));
+        cudaEvent_t e0, e1;
+        TKV_CUDA_CHECK(cudaEventCreate(&e0));
+        TKV_CUDA_CHECK(cudaEventCreate(&e1));
+        double gemm_ms = 0, gemm_fl = 0, gath_ms = 0, attn_ms = 0, gath_b = 0;
+        model.set_timing(s->encode_timed);
+        long launches = 0, tokens_total = 0, tables_total = 0;
+        TKV_CUDA_CHECK(cudaEventRecord(e0, st));
+        tkv::StagingRing& ring = model.ring();
+        for (const auto& bt : batches) {
+            std::vector<int32_t> toks, pos, grp;
+            std::vector<tkv::AttnSeq> seqs;
+            for (int gi : bt) {
+                const int row0 = int(toks.size());
+                for (int t : e.plan.groups[size_t(gi)].tables)
+                    toks.insert(toks.end(), e.table_tokens[size_t(t)].begin(), e.table_tokens[size_t(t)].end());
+                const int n = int(toks.size()) - row0;
+                for (int i = 0; i < n; ++i) pos.push_back(i), grp.push_back(0);
+                seqs.push_back({row0, n, 0, 0});
+            }
+            const int M = int(toks.size());
+            std::vector<int64_t> pos64(pos.begin(), pos.end());
+            int max_pos = 0;
+            for (int gi : bt) max_pos = std::max(max_pos, gsz[size_t(gi)]);
+            model.rope().ensure(max_pos + 2);
+            tkv::FwdArgs fa;
+            fa.M = M;
+            fa.tokens = static_cast<const int32_t*>(ring.upload(toks.data(), toks.size() * 4, st));
+            fa.pos = static_cast<const int32_t*>(ring.upload(pos.data(), pos.size() * 4, st));
+            fa.pos64 = static_cast<const int64_t*>(ring.upload(pos64.data(), pos64.size() * 8, st));
+            fa.group = static_cast<const int32_t*>(ring.upload(grp.data(), grp.size() * 4, st));
+            fa.group_host = grp.data();
+            fa.n_seqs = int(seqs.size());
+            fa.seqs = static_cast<const tkv::AttnSeq*>(ring.upload(seqs.data(), seqs.size() * sizeof(tkv::AttnSeq), st));
+            fa.seqs_host = seqs.data();
+            fa.mode = 1;
+            fa.kraw_out = dk;
+            fa.v_out = dv;
+            model.forward(fa, st);
+            launches += model.launches();
+            tokens_total += M;
+            // each table's rows [row0 + off, +T) of every layer -> its image ([K: L][T] then [V: L][T])
+            for (size_t si = 0; si < bt.size(); ++si) {
+                const auto& g = e.plan.groups[size_t(bt[si])];
+                for (size_t i = 0; i < g.tables.size(); ++i) {
+                    const int t = g.tables[i], off = g.offsets[i], T = int(e.table_tokens[size_t(t)].size());
+                    const tkv::TableImage* img = s->arena->find(t);
+                    if (img && (img->dtype != img_dt || img->tokens != T || img->layers != L || img->kv_dim != kvd))
+                        continue;  // a loaded image of another format stays as it is
+                    if (!img) img = &s->arena->put(t, T, L, kvd, off, img_dt, nullptr);
+                    const size_t src0 = (size_t(seqs[si].q_row0) + size_t(off)) * row;
+                    for (int kvi = 0; kvi < 2; ++kvi)
+                        TKV_CUDA_CHECK(cudaMemcpy2DAsync(img->host + size_t(kvi) * L * T * row, size_t(T) * row,
+                                                         static_cast<const uint8_t*>(kvi ? dv : dk) + src0, size_t(M) * row,
+                                                         size_t(T) * row, size_t(L), cudaMemcpyDeviceToHost, st));
+                    ++tables_total;
+                }
+            }
+            // the host vectors above back the staging uploads and group_host: drain before reuse
+            TKV_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        TKV_CUDA_CHECK(cudaEventRecord(e1, st));
+        TKV_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0;
+        TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (s->encode_timed) model.collect_timing(gemm_ms, gemm_fl, gath_ms, attn_ms, gath_b);
+        model.set_timing(false);
+        s->encode_stats = {double(e.plan.groups.size()), double(tables_total), double(tokens_total), double(batches.size()),
+                           double(ms), gemm_ms, gemm_fl, attn_ms, double(launches)};
+        if (out_dir) {
+            for (const auto& g : e.plan.groups)
+                for (int t : g.tables) {
+                    const tkv::TableImage* img = s->arena->find(t);
+                    if (!img || img->dtype != img_dt) continue;
                     std::string file;
-                    for (int fld : {t, T, L, c.kv_heads, c.head_dim, off}) tablekv::kvfile::le32(file, std::uint32_t(fld));
-                    file.append(reinterpret_cast<const char*>(img.data()), img.size());
+                    for (int fld : {t, img->tokens, L, c.kv_heads, c.head_dim, img->local_offset})
+                        tablekv::kvfile::le32(file, std::uint32_t(fld));
+                    file.append(reinterpret_cast<const char*>(img->host), img->bytes);
                     const auto name = std::to_string(t) + (img_dt == tkv::DType::f32 ? ".kv" : ".kvb");
                     std::ofstream of(tmp / name, std::ios::binary);
                     of.write(file.data(), std::streamsize(file.size()));
                     if (!of) throw tablekv::Error(tablekv::Errc::io_error, "short write on " + (tmp / name).string());
                 }
-            }
-        }
-        if (out_dir) {
             std::ofstream mf(tmp / "manifest.json", std::ios::binary);
             mf << tablekv::manifest_json(e);
             mf.close();
@@ -746,6 +849,14 @@ int tkv_store_precompute(tkv_store* s, const tkv_engine* eh, const char* out_dir
             fs::remove_all(out_dir, ec);
             fs::rename(tmp, out_dir);
         }
+    });
+}
+
+int tkv_store_precompute_stats(const tkv_store* s, int timed_next, double* out, int n) {
+    return guard([&] {
+        need(s != nullptr, "null argument");
+        const_cast<tkv_store*>(s)->encode_timed = timed_next != 0;
+        for (int i = 0; out && i < n && i < int(s->encode_stats.size()); ++i) out[i] = s->encode_stats[size_t(i)];
     });
 }
 

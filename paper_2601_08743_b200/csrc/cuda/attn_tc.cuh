@@ -29,6 +29,11 @@ struct AttnArgs {
     int n_segs = 0;
     int prefetch = 0;                    // tiles ahead pulled into L2 (0 = off)
     long k_hm_rows = 0;                  // > 0: k_ctx is head-major [kv head][k_hm_rows][head_dim]
+    // paged K (with vpool): cached-prefix K rows also come straight from the pages, rotated in
+    // shared memory at their prefix positions with the f32 RoPE tables [pos][head_dim/2]
+    bool kpaged = false;
+    const float* cos_f = nullptr;
+    const float* sin_f = nullptr;
     const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row
                                       // (start of the row's group block; 0 for query rows)
 };

@@ -9,6 +9,11 @@
 // from one item into the next.
 // Warp 0: TMA lanes (lane 0: the item's two Q tiles + K tiles, lane 16: V tiles; 2-deep rings of
 // 32 KB tiles) from the prefix slab or the own-row buffer (a tile never straddles the two).
+// Paged prefix (the serving path): cached-prefix tiles come straight from the tables' pool pages,
+// no slab at all — V by warps 2-3 (16-byte cp.async into the swizzled tile), K by warpgroup 3
+// (warps 12-15, one per SM sub-partition): 16-byte cp.async of the raw rows, then RoPE applied in
+// place in shared memory (assemble's rotation at the key's prefix position, attention.hpp:300-362)
+// before the tile is handed to the tensor core. Own-row tiles (already rotated) stay on TMA.
 // Warp 1: MMA issuer, order PV_0(t) QK_0(t+1) PV_1(t) QK_1(t+1): S_s = Q_s.K^T (SS) into TMEM, then
 // O_s += P_s.V with P_s read from TMEM (TS: the A operand stays in tensor memory, so P never
 // touches shared memory and each PV reads only V from smem).
@@ -35,9 +40,12 @@ namespace tkv {
 namespace {
 
 constexpr int BM = 128, BN = 128, D = 128;
-constexpr int kThreads = 384;  // warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); warpgroups 1 / 2: softmax of Q0 / Q1
+// warpgroup 0: warp 0 TMA, warp 1 MMA, warps 2-3 paged V; warpgroups 1 / 2: softmax of Q0 / Q1;
+// warpgroup 3: paged K (load + rotate)
+constexpr int kThreads = 512;
+constexpr int kKLoadThreads = 128, kVLoadThreads = 64;
 #ifndef TKV_ATTN_KSTAGES
-#define TKV_ATTN_KSTAGES 2
+#define TKV_ATTN_KSTAGES 3  // three K slots: the paged-K loader rotates tile g-1 while tile g lands
 #endif
 #ifndef TKV_ATTN_VSTAGES
 #define TKV_ATTN_VSTAGES 2
@@ -86,9 +94,6 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint3
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int x, int y) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y)
                  : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -223,6 +228,36 @@ __host__ __device__ constexpr uint32_t idesc(bool b_mn, int n) {
 }
 
 
+// Walks the window's table segments along increasing prefix rows: the page address of one head's
+// 256-byte row of a cached table image ([K: L][T][kv_dim] then [V: L][T][kv_dim], table_kv.hpp:45-48)
+// for layer slot `ls` (l for K, L + l for V). Rows only grow along a CTA's walk through an item, so
+// each lookup advances the cursor instead of searching (one binary search per item).
+struct SegCursor {
+    int seg, next_row0;  // current segment; first row of the next one (INT_MAX past the end)
+    GatherSeg sg;
+    __device__ __forceinline__ void seek(const AttnArgs& a, int vr) {
+        int lo = 0, hi = a.n_segs - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (a.segs[mid].out_row0 <= vr) lo = mid; else hi = mid - 1;
+        }
+        seg = lo;
+        sg = a.segs[lo];
+        next_row0 = lo + 1 < a.n_segs ? a.segs[lo + 1].out_row0 : 0x7fffffff;
+    }
+    __device__ __forceinline__ const uint8_t* row(const AttnArgs& a, int vr, int ls, int kvh) {
+        while (vr >= next_row0) {
+            ++seg;
+            sg = a.segs[seg];
+            next_row0 = seg + 1 < a.n_segs ? a.segs[seg + 1].out_row0 : 0x7fffffff;
+        }
+        const long row_bytes = long(a.kv_heads) * 128 * 2;
+        const long off = (long(ls) * sg.tokens + (vr - sg.out_row0)) * row_bytes + long(kvh) * 128 * 2;
+        return a.vpool + (long(__ldg(a.page_ids + sg.page_off + (off >> a.page_shift))) << a.page_shift) +
+               (off & ((1L << a.page_shift) - 1));
+    }
+};
+
 struct Tc5Args {
     AttnArgs a;
     const int4* work;  // {seq, tok0, kvh, 0}, tok0 a multiple of 2·BM/G, heaviest first
@@ -284,10 +319,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_pvdone(st), 1);
             mbar_init(b_ofree(st), 4);
         }
-        for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), 1), mbar_init(b_kempty(i), 1);
+        // K tiles: 1 arrival (TMA lane) or, with paged K, all of warpgroup 3 (own-row tiles: one
+        // thread arms the TMA transaction, the rest arrive plainly)
+        for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), a.kpaged ? kKLoadThreads : 1), mbar_init(b_kempty(i), 1);
         // V tiles come from the TMA lane (1 arrival) or, with paged V, from warps 2-3 (64 arrivals;
         // for own-row tiles one of them arms the TMA transaction and the rest arrive plainly)
-        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), a.vpool ? 64 : 1), mbar_init(b_vempty(i), 1);
+        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), a.vpool ? kVLoadThreads : 1), mbar_init(b_vempty(i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -337,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                it.sq.q_row0 + it.tok0 + st * TQ);
                 }
                 TR(8, j);
+                if (a.kpaged) continue;  // K tiles come from warpgroup 3
                 auto prefetch_kv = [&](int t) {  // K always; V here only when it comes by TMA
                     bool ctx;
                     const int row = tile_row(it, t, ctx);
@@ -381,54 +419,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if ((warp == 2 || warp == 3) && a.vpool) {
         // ---- paged V: cached-prefix tiles copied from the table pages with 16-byte cp.async into
-        // the swizzled tile (each of the 64 threads owns two key rows), own-row tiles by TMA
+        // the swizzled tile; 16 threads per 256-byte head row (two whole rows per warp instruction,
+        // every L2 sector fetched once), own-row tiles by TMA
         const int tid = threadIdx.x - 64;
-        const long row_bytes = long(a.kv_heads) * D * 2;
-        const long pmask = (1L << a.page_shift) - 1;
-        // The V row of prefix key `key` inside its table's pages. Keys only grow along a CTA's walk
-        // through an item, so each lookup advances a per-thread segment cursor (one binary search
-        // per item) and remembers the last page, instead of searching per row.
-        struct VCur {
-            int seg, next_row0;  // current segment; first row of the next one (INT_MAX past the end)
-            GatherSeg sg;
-        };
-        auto v_seek = [&](VCur& c, int vr) {  // binary search: the segment holding window row vr
-            int lo = 0, hi = a.n_segs - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (a.segs[mid].out_row0 <= vr) lo = mid; else hi = mid - 1;
-            }
-            c.seg = lo;
-            c.sg = a.segs[lo];
-            c.next_row0 = lo + 1 < a.n_segs ? a.segs[lo + 1].out_row0 : 0x7fffffff;
-        };
-        auto v_src = [&](VCur& c, const Item& it, int key) {
-            const int vr = it.sq.ctx_row0 + key;  // window ctx row -> its table segment
-            while (vr >= c.next_row0) {
-                ++c.seg;
-                c.sg = a.segs[c.seg];
-                c.next_row0 = c.seg + 1 < a.n_segs ? a.segs[c.seg + 1].out_row0 : 0x7fffffff;
-            }
-            const long off = ((long(a.layers) + a.layer) * c.sg.tokens + (vr - c.sg.out_row0)) * row_bytes + long(it.kvh) * D * 2;
-            return a.vpool + (long(__ldg(a.page_ids + c.sg.page_off + (off >> a.page_shift))) << a.page_shift) + (off & pmask);
-        };
-        const int pf = a.prefetch;
-        VCur cl, cp;  // load cursor, prefetch cursor
-        auto prefetch_v = [&](const Item& it, int t) {
-            if (t >= it.n_ctx_tiles) return;  // own tiles: the TMA lane prefetches them
-            for (int rr = tid; rr < BN; rr += 64)
-                if (t * BN + rr < it.sq.n_ctx) bulk_prefetch(v_src(cp, it, t * BN + rr), D * 2);
-        };
+        const int c = tid & 15, sub = tid >> 4;  // chunk of the head row, row phase (rows sub + 4i)
+        SegCursor cur;
         long g = 0;
         for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
             const Item it = item(w);
-            if (it.n_ctx_tiles) {
-                v_seek(cl, it.sq.ctx_row0);
-                cp = cl;
-            }
-            for (int t = kVStages; t < min(pf, it.n_tiles); ++t) prefetch_v(it, t);
+            if (it.n_ctx_tiles) cur.seek(a, it.sq.ctx_row0);
             for (int t = 0; t < it.n_tiles; ++t, ++g) {
-                if (pf && t + pf < it.n_tiles) prefetch_v(it, t + pf);
                 const int sv = int(g % kVStages);
                 mbar_wait(b_vempty(sv), int((g / kVStages) & 1) ^ 1);
                 if (tid == 0) TR(1, g);
@@ -444,25 +444,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     continue;
                 }
-                for (int rr = tid; rr < BN; rr += 64) {
+                bool zeros = false;
+                for (int rr = sub; rr < BN; rr += kVLoadThreads / 16) {
                     const int key = t * BN + rr;  // key index within this sequence's prefix
+                    const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
                     if (key < it.sq.n_ctx) {
-                        const uint8_t* src = v_src(cl, it, key);
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + c * 16) : "memory");
-                        }
+                        const uint8_t* src = cur.row(a, it.sq.ctx_row0 + key, a.layers + a.layer, it.kvh) + c * 16;
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
                     } else {  // past the prefix: finite zeros (masked in the softmax)
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-                            asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
+                        zeros = true;
                     }
                 }
+                if (zeros) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(b_vfull(sv)) : "memory");
+                if (tid == 0) TR(15, g);
             }
         }
     } else if (warp == 1) {
@@ -491,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (st == 0) {
                     mbar_wait(b_kfull(sk), int((c.gi / kKStages) & 1));
                     TR(2, c.gi);
+                    if (a.kpaged) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // rotated rows -> tensor core
                 }
                 if (c.t == 0) mbar_wait(b_qfull(st), c.j & 1);
                 fence_after();
@@ -542,8 +539,102 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
+    } else if (warp >= 12) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+        if (a.kpaged) {
+            // ---- paged K: raw rows by 16-byte cp.async into the swizzled ring slot (16 threads per
+            // 256-byte head row), then each thread rotates the chunks it loaded in place: interleaved
+            // pairs k = 4c..4c+3 at the key's prefix position p (assemble, attention.hpp:300-362),
+            // a' = a cos - b sin, b' = a sin + b cos in f32 and rounded to bf16 (the gather's formula).
+            // cos/sin of p come from the f32 table at the thread's first row of the tile and advance
+            // by R(8 theta_k) per row step (8 rows apart): no table traffic per row. One tile of
+            // lookahead: tile g's loads are issued before tile g-1 is rotated and published.
+            const int kt = threadIdx.x - 384;
+            const int c = kt & 15, sub = kt >> 4;  // chunk of the head row, row phase (rows sub + 8i)
+            constexpr int kRowStep = kKLoadThreads / 16;
+            const int half = D / 2;
+            float cd[4], sd[4];  // R(kRowStep theta_k), k = 4c..4c+3
+            {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + kRowStep * half + 4 * c));
+                const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + kRowStep * half + 4 * c));
+                cd[0] = x.x, cd[1] = x.y, cd[2] = x.z, cd[3] = x.w;
+                sd[0] = y.x, sd[1] = y.y, sd[2] = y.z, sd[3] = y.w;
+            }
+            SegCursor cur;
+            struct Pend {
+                int slot, tile, n_ctx;  // tile < 0: nothing to rotate
+            } pend{0, -1, 0};
+            auto finish = [&](const Pend& p) {  // rotate a landed ctx tile in place and publish it
+                if (p.tile < 0) return;
+                const uint32_t dk = s0 + kK0 + p.slot * kKVTile;
+                const int pos0 = p.tile * BN + sub;
+                if (pos0 < p.n_ctx) {
+                    float cs[4], sn[4];
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + long(pos0) * half + 4 * c));
+                    const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + long(pos0) * half + 4 * c));
+                    cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
+                    sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
+                    for (int rr = sub; rr < BN && p.tile * BN + rr < p.n_ctx; rr += kRowStep) {
+                        const uint32_t at = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                        uint32_t w[4];
+                        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(at));
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float x0 = __uint_as_float(w[j] << 16), x1 = __uint_as_float(w[j] & 0xffff0000u);
+                            w[j] = pack_bf16x2(fmaf(x0, cs[j], -x1 * sn[j]), fmaf(x0, sn[j], x1 * cs[j]));
+                            const float cn = fmaf(cs[j], cd[j], -sn[j] * sd[j]);
+                            sn[j] = fmaf(sn[j], cd[j], cs[j] * sd[j]);
+                            cs[j] = cn;
+                        }
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                                     : "memory");
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(b_kfull(p.slot));
+            };
+            long g = 0;
+            for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
+                const Item it = item(w);
+                if (it.n_ctx_tiles) cur.seek(a, it.sq.ctx_row0);
+                for (int t = 0; t < it.n_tiles; ++t, ++g) {
+                    const int sk = int(g % kKStages);
+                    mbar_wait(b_kempty(sk), int((g / kKStages) & 1) ^ 1);
+                    if (kt == 0) TR(0, g);
+                    bool ctx;
+                    const int row = tile_row(it, t, ctx);
+                    const uint32_t dk = s0 + kK0 + sk * kKVTile;
+                    if (!ctx) {  // own rows: rotated by the QKV epilogue, one TMA transaction
+                        if (kt == 0) {
+                            mbar_expect_tx(b_kfull(sk), kKVTile);
+                            for (int h = 0; h < 2; ++h) tma_2d(dk + h * kKVHalf, &mk_own, b_kfull(sk), it.kvh * D + h * 64, row);
+                        } else {
+                            mbar_arrive(b_kfull(sk));
+                        }
+                    } else {
+                        for (int rr = sub; rr < BN; rr += kRowStep) {
+                            const int key = t * BN + rr;
+                            const uint32_t dst = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                            if (key < it.sq.n_ctx) {
+                                const uint8_t* src = cur.row(a, it.sq.ctx_row0 + key, a.layer, it.kvh) + c * 16;
+                                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                            } else {
+                                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
+                            }
+                        }
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");  // the previous tile's rows have landed
+                    finish(pend);
+                    if (kt == 0 && g > 0) TR(9, g - 1);
+                    pend = ctx ? Pend{sk, t, it.sq.n_ctx} : Pend{0, -1, 0};
+                }
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            finish(pend);
+        }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
         // ---- softmax: stream st = Q tile, lane quarter q4 = warp % 4 (TMEM lanes = rows); every
         // thread owns one query row and all 128 columns of each S tile
         const int st = (warp - 4) >> 2, q4 = warp & 3;

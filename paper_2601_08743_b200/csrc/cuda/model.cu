@@ -287,7 +287,10 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         const char* e = std::getenv("TKV_K_HEAD_MAJOR");
         return !(e && std::atoi(e) == 0);
     }();
-    const bool k_head_major = paged_v && hm_env && gather_use_tma();
+    // paged K: the attention's loader warps read K from the pages too and rotate it in smem, so
+    // no gather runs and no K slab is written or re-read
+    const bool paged_k = paged_v && a.paged_k;
+    const bool k_head_major = paged_v && !paged_k && hm_env && gather_use_tma();
     const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
@@ -342,7 +345,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.k_own = static_cast<const __nv_bfloat16*>(k);
         aa.v_own = static_cast<const __nv_bfloat16*>(v_l);
         const bool streamed = a.gather_segs != nullptr;
-        if (streamed) {
+        if (streamed && !paged_k) {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing_) {
                 e0 = timing_event();
@@ -396,6 +399,9 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             aa.n_segs = a.gather_n_segs;
             aa.layer = l;
             aa.layers = c.num_layers;
+            aa.kpaged = paged_k;
+            aa.cos_f = rope_.cos_f();
+            aa.sin_f = rope_.sin_f();
         }
         {
             cudaEvent_t e0 = nullptr, e1 = nullptr;

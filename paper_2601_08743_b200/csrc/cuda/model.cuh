@@ -88,6 +88,7 @@ struct FwdArgs {
     int gather_n_segs = 0, gather_rows = 0;
     const int4* gather_chunks = nullptr;    // device: {seg, t0, rows, 0} (bf16 fast path)
     bool paged_v = false;                   // tcgen05 attention reads prefix V from the pages (gather: K only)
+    bool paged_k = false;                   // ... and K too, rotated in shared memory (no gather, no slab)
     int gather_n_chunks = 0;
     DType gather_in = DType::bf16;
     void* kraw_out = nullptr;           // optional [L][M][kv_dim] pre-rotation keys (offline encode)

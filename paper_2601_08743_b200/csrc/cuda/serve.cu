@@ -607,6 +607,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                     return !(e && std::string(e) == "0");
                 }();
                 fa.paged_v = paged_v;
+                static const bool paged_k = [] {  // TKV_PAGED_K=0 gathers rotated K into a slab (A/B)
+                    const char* e = std::getenv("TKV_PAGED_K");
+                    return !(e && std::string(e) == "0");
+                }();
+                fa.paged_k = paged_k;
             }
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
             fa.logit_rows_host = logit_rows.data();

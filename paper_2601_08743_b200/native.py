@@ -92,6 +92,7 @@ _sig("tkv_store_put", _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp)
 _sig("tkv_store_load_kv_file", _vp, C.c_char_p, C.POINTER(C.c_int))
 _sig("tkv_store_load_dir", _vp, C.c_char_p, _vp, C.c_int, C.POINTER(C.c_int))
 _sig("tkv_store_precompute", _vp, _vp, C.c_char_p)
+_sig("tkv_store_precompute_stats", _vp, C.c_int, C.POINTER(C.c_double), C.c_int)
 _sig("tkv_store_fetch", _vp, C.c_int, C.c_int, _vp, C.c_size_t)
 _sig("tkv_store_assemble", _vp, _i32p, C.c_int, C.c_size_t, _vp, _vp, C.POINTER(C.c_int))
 _sig("tkv_store_info", _vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
@@ -399,8 +400,15 @@ class Store:
         _check(_lib.tkv_store_load_dir(self._h, path.encode(), engine._h if engine else None, threads, C.byref(n)))
         return n.value
 
-    def precompute(self, engine: Engine, out_dir=None):
+    def precompute(self, engine: Engine, out_dir=None, timed=False):
+        """Offline encode of every group on the GPU (batched block-causal forwards) into the arena;
+        returns the encode stats (timed=True adds CUDA-event GEMM / attention times)."""
+        _check(_lib.tkv_store_precompute_stats(self._h, int(timed), None, 0))
         _check(_lib.tkv_store_precompute(self._h, engine._h, out_dir.encode() if out_dir else None))
+        v = (C.c_double * 9)()
+        _check(_lib.tkv_store_precompute_stats(self._h, 0, v, 9))
+        keys = ("groups", "tables", "tokens", "forwards", "device_ms", "gemm_ms", "gemm_flops", "attn_ms", "launches")
+        return dict(zip(keys, list(v)))
 
     def bind_engine(self, engine: Engine):
         _check(_lib.tkv_store_bind_engine(self._h, engine._h))

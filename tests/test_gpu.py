@@ -136,6 +136,44 @@ def test_precompute_encode_matches_reference_kv_files(f32_model, tmp_path):
     s.close()
 
 
+_ENCODE_SCRIPT = r"""
+import sys
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+from paper_2601_08743_b200 import native as N
+from golden_util import demo_path
+kw = dict(num_layers=2, num_heads=4, head_dim=16, vocab_size=330) if sys.argv[3] == 'f32' else \
+    dict(num_layers=2, num_heads=8, num_kv_heads=2, head_dim=128, vocab_size=330, ffn_dim=512, mlp='swiglu', norm='rms')
+m = N.Model(dtype=sys.argv[3], **kw)
+s = N.Store(m, page_bytes=64 << 10, n_pages=256)
+st = s.precompute(N.Engine(demo_path('demo_schema.json')), sys.argv[2])
+print(int(st['forwards']), int(st['tokens']))
+s.close(); m.close()
+"""
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_batched_encode_identical_to_one_forward_per_group(tmp_path, dtype):
+    """The batched offline encode (groups packed into block-causal forwards) writes the same image
+    bytes as one forward per group (TKV_ENCODE_ROWS=1): rows never see another group's rows."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for rows in ("1", "16384"):
+        d = tmp_path / ("enc" + rows)
+        env = dict(os.environ, TKV_ENCODE_ROWS=rows)
+        r = subprocess.run([sys.executable, "-c", _ENCODE_SCRIPT, root, str(d), dtype], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[rows] = (d, [int(x) for x in r.stdout.split()])
+    (d1, (f1, n1)), (d2, (f2, n2)) = outs["1"], outs["16384"]
+    assert n1 == n2 and f1 > f2 == 1  # per-group forwards vs one batched forward
+    names = sorted(os.listdir(d1))
+    assert names == sorted(os.listdir(d2)) and len(names) == 13  # 12 tables + manifest
+    for nm in names:
+        assert open(d1 / nm, "rb").read() == open(d2 / nm, "rb").read(), nm
+
+
 @pytest.mark.parametrize("shape", [(128, 128, 64), (200, 192, 64), (1, 256, 4096), (517, 512, 1000),
                                    (4096, 1024, 4096), (300, 6144, 256), (1000, 28672, 64)])
 def test_tcgen05_gemm_vs_numpy(shape):
@@ -481,21 +519,39 @@ s.close(); m.close()
 """
 
 
-@pytest.mark.parametrize("variant", [{"TKV_PAGED_V": "0"}, {"TKV_K_HEAD_MAJOR": "0"}])
-def test_paged_v_and_head_major_k_bit_identical_to_slab(tmp_path, variant):
-    """Paged V (the attention reads V straight from the pool pages) and the head-major K slab move
-    the same bytes to the same smem tiles as the gathered row-major slab: the served logits must be
-    bit-identical, not merely within tolerance."""
+def _paged_logits(tmp_path, tag, env_over):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = []
-    for i, env_over in enumerate([{}, variant]):
-        out = str(tmp_path / ("logits%d.npy" % i))
-        env = dict(os.environ, **env_over)
-        p = subprocess.run([sys.executable, "-c", _PAGED_SCRIPT, root, out], env=env, capture_output=True, text=True,
-                           timeout=600)
-        assert p.returncode == 0, p.stderr[-2000:]
-        outs.append(np.load(out))
-    assert outs[0].shape == outs[1].shape and np.isfinite(outs[0]).all()
-    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    out = str(tmp_path / ("logits_%s.npy" % tag))
+    p = subprocess.run([sys.executable, "-c", _PAGED_SCRIPT, root, out], env=dict(os.environ, **env_over),
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("variant", [{"TKV_PAGED_V": "0"}, {"TKV_K_HEAD_MAJOR": "0"}])
+def test_paged_v_and_head_major_k_bit_identical_to_slab(tmp_path, variant):
+    """With the rotated-K gather (TKV_PAGED_K=0): paged V (the attention reads V straight from the
+    pool pages) and the head-major K slab move the same bytes to the same smem tiles as the
+    gathered row-major slab: the served logits must be bit-identical, not merely within tolerance."""
+    base = _paged_logits(tmp_path, "base", {"TKV_PAGED_K": "0"})
+    other = _paged_logits(tmp_path, "var", dict(variant, TKV_PAGED_K="0"))
+    assert base.shape == other.shape and np.isfinite(base).all()
+    assert np.array_equal(base.view(np.uint32), other.view(np.uint32))
+
+
+def test_paged_k_rotated_in_smem_matches_gathered_slab(tmp_path):
+    """Paged K (default: raw K rows copied from the pages into the attention's smem ring and rotated
+    there, cos/sin advanced by a per-thread angle recurrence from the f32 table) against the
+    gathered, table-rotated K slab: a rotated element can differ by one bf16 ulp where the
+    recurrence's ~1e-6 relative drift crosses a rounding boundary, so logits agree to 1e-2 (not
+    bit-exact) and the first token is the same wherever the slab's top-2 margin exceeds 2e-2."""
+    paged = _paged_logits(tmp_path, "paged", {})[:, :330]
+    slab = _paged_logits(tmp_path, "slab", {"TKV_PAGED_K": "0"})[:, :330]
+    assert paged.shape == slab.shape and np.isfinite(paged).all()
+    assert np.abs(paged - slab).max() <= 1e-2
+    top2 = np.sort(slab, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 2e-2
+    assert clear.sum() >= len(clear) // 2
+    assert np.array_equal(paged.argmax(1)[clear], slab.argmax(1)[clear])
