@@ -408,6 +408,16 @@ def main():
     copy_ms = sum(r["copy_busy_ms"] for r in results) / args.steps
     dem_b = sum(r["h2d_demand_bytes"] for r in results) / args.steps
     dem_ms = sum(r["copy_demand_ms"] for r in results) / args.steps
+    # attention work of this rank's queries (algorithmic): per layer 4 * q_heads * head_dim FLOP per
+    # (query row, visible key) and the cached prefix's K + V read once per (query, kv head)
+    ttok = [len(x) for x in eng.info["table_tokens"]]
+    attn_fl = attn_kv_b = 0.0
+    if not c1:
+        for i in my_slice(global_order()):
+            p_ = sum(ttok[t] for t in analyzed[i]["assembly_order"])
+            s_ = len(analyzed[i]["remainder"])
+            attn_fl += 4.0 * mk["num_heads"] * mk["head_dim"] * s_ * (p_ + (s_ + 1) / 2.0) * mk["num_layers"]
+            attn_kv_b += 2.0 * p_ * mk["num_kv_heads"] * mk["head_dim"] * 2 * mk["num_layers"]
     gemm_ms = sum(r["gemm_ms"] for r in results)
     gemm_fl = sum(r["gemm_flops"] for r in results)
     launches = sum(r["launches"] for r in results)
@@ -457,7 +467,10 @@ def main():
             t = time.perf_counter()
             N.rerank_device(sets8, n_bits, seed=1, device=local)
             ts.append((time.perf_counter() - t) * 1e3)
-        rr8 = {"queries": len(sets8), "ms": min(ts), "ms_all": [round(x, 2) for x in ts]}
+        rr8 = {"queries": len(sets8), "ms": min(ts), "ms_all": [round(x, 2) for x in ts],
+               "breakdown_last_call": N.rerank_device_stats(),
+               "what": "rerank_device wall clock: incidence packing + host reduction to distinct table sets + H2D + "
+                       "the cluster chain kernel (CUDA events: kernel_ms) + D2H + expansion"}
 
     if rank != 0:
         if world > 1:
@@ -528,7 +541,8 @@ def main():
                    "gbs": (sum(r["gather_bytes"] for r in results) / (sum(r["gather_ms"] for r in results) / 1e3) / 1e9
                            if sum(r["gather_ms"] for r in results) else None),
                    "peak_gbs": peaks.get("hbm_gbs"),
-                   "bytes_definition": "prefix rows x layers x kv_dim x (read + write element bytes) for K (rotated into the slab); V is read by the attention straight from the pages (paged V; TKV_PAGED_V=0 gathers V too and counts it)"},
+                   "bytes_definition": "slab mode only (TKV_PAGED_K=0): prefix rows x layers x kv_dim x 2 x (read + "
+                                       "write element bytes); the default paged prefix runs no gather (0 ms)"},
         "global_rerank_ms_per_step": sum(timed_rerank_ms) / args.steps,
         "global_rerank_at_8x": rr8,
         "encode": {"what": "offline table encode (precompute_corpus) on the GPU: every group as one block-causal "
@@ -543,6 +557,17 @@ def main():
                    "flops_frac_of_peak_over_device_time": (enc["gemm_flops"] / (enc["device_ms"] / 1e3) / 1e12) / peak_tf
                    if enc["device_ms"] else None},
         "attention_ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
+        "attention": {"kernel": "attn_tc5 (tcgen05/TMEM; paged prefix: K/V TMA'd from the pool pages, K rotated in smem)",
+                      "ms_per_step": sum(r["attn_ms"] for r in results) / args.steps,
+                      "tflops": attn_fl / (sum(r["attn_ms"] for r in results) / args.steps / 1e3) / 1e12
+                      if not c1 and sum(r["attn_ms"] for r in results) else None,
+                      "frac_of_bf16_peak": attn_fl / (sum(r["attn_ms"] for r in results) / args.steps / 1e3) / 1e12 / peak_tf
+                      if not c1 and sum(r["attn_ms"] for r in results) else None,
+                      "prefix_kv_gbs": attn_kv_b / (sum(r["attn_ms"] for r in results) / args.steps / 1e3) / 1e9
+                      if not c1 and sum(r["attn_ms"] for r in results) else None,
+                      "flops_per_step": attn_fl, "prefix_kv_bytes_per_step": attn_kv_b,
+                      "definition": "flops = 4 * q_heads * head_dim * suffix * (prefix + (suffix+1)/2) * layers per "
+                                    "query; bytes = the prefix's K and V (bf16) once per query and layer"},
         "e2e": {"value": len(e2e_texts) * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h, "p50_ttft_ms": pct(e2e_res["ttft_ms"], 0.5),
                 "last_step_ms": {"prompt_analysis": e2e_res.get("analyze_ms"), "host_enqueue": e2e_res["host_ms"],

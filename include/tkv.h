@@ -68,9 +68,13 @@ int tkv_trie_match_all(const tkv_trie* t, const int32_t* tokens, size_t n, int64
 /* inc: [n][words] packed incidence bitsets; perm_out: n indices; threads 0 = auto */
 int tkv_rerank(const uint64_t* inc, size_t n, size_t words, uint64_t seed, int fixed_first, int threads,
                uint64_t* perm_out);
-/* the same permutation computed on GPU `device` (one CTA runs the greedy chain; bit-exact) */
+/* the same permutation computed on GPU `device` (one thread-block cluster runs the greedy chain over
+ * the distinct table sets; bit-exact) */
 int tkv_rerank_device(int device, const uint64_t* inc, size_t n, size_t words, uint64_t seed, int fixed_first,
                       uint64_t* perm);
+/* the calling thread's last tkv_rerank_device: out = {host class reduction ms, chain kernel ms (CUDA
+ * events), whole call ms, distinct table sets, cluster CTAs} */
+int tkv_rerank_device_stats(double* out, int n);
 
 /* ---- fast-tier policy bookkeeping (tiered_cache.hpp:69-113) over a metadata slow tier --- */
 typedef struct tkv_cache tkv_cache;

@@ -384,6 +384,15 @@ int tkv_rerank_device(int device, const uint64_t* inc, size_t n, size_t words, u
     });
 }
 
+int tkv_rerank_device_stats(double* out, int n) {
+    return guard([&] {
+        need(out || n == 0, "null argument");
+        const tkv::RerankStats st = tkv::last_rerank_stats();
+        const double v[5] = {st.classes_ms, st.kernel_ms, st.total_ms, st.n_classes, double(st.cluster)};
+        for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+    });
+}
+
 // ------------------------------------------------------------------ cache
 int tkv_cache_create(size_t capacity, int policy, const int32_t* counts, size_t n, tkv_cache** out) {
     return guard([&] {

@@ -20,18 +20,20 @@ struct AttnArgs {
     __nv_bfloat16* out;          // [M][Hq*d]
     int num_heads, kv_heads, head_dim, mode;
     float scale;                 // 1/sqrt(d)
-    // paged V (tcgen05 kernel, cached prefix): when vpool is set, the V rows of cached-prefix
-    // tiles are copied straight from the table pages (the gather only materialises rotated K)
-    const uint8_t* vpool = nullptr;
+    const uint8_t* vpool = nullptr;      // paged mode: pool base (below)
+    long pool_rows = 0;                  // paged mode: pool bytes / (kv_heads * head_dim * 2)
     int page_shift = 0, layer = 0, layers = 0;
     const int32_t* page_ids = nullptr;   // window page-id list (GatherSeg::page_off indexes it)
     const GatherSeg* segs = nullptr;     // window segments, ascending out_row0 (= ctx rows)
     int n_segs = 0;
     int prefetch = 0;                    // tiles ahead pulled into L2 (0 = off)
     long k_hm_rows = 0;                  // > 0: k_ctx is head-major [kv head][k_hm_rows][head_dim]
-    // paged K (with vpool): cached-prefix K rows also come straight from the pages, rotated in
-    // shared memory at their prefix positions with the f32 RoPE tables [pos][head_dim/2]
+    // paged prefix (tcgen05 kernel): cached-prefix K and V rows come straight from the table pages
+    // by TMA over the pool (rows of kv_heads * head_dim bf16, 2^rows_shift rows per page) and K is
+    // rotated in shared memory at its prefix positions with the f32 RoPE tables [pos][head_dim/2];
+    // vpool = pool base, page_ids / segs / layer / layers locate the rows, no slab
     bool kpaged = false;
+    int rows_shift = 0;
     const float* cos_f = nullptr;
     const float* sin_f = nullptr;
     const int32_t* row_lo = nullptr;  // mode 1 on the tcgen05 kernel: first visible own key per row

@@ -40,10 +40,10 @@ namespace tkv {
 namespace {
 
 constexpr int BM = 128, BN = 128, D = 128;
-// warpgroup 0: warp 0 TMA, warp 1 MMA, warps 2-3 paged V; warpgroups 1 / 2: softmax of Q0 / Q1;
-// warpgroup 3: paged K (load + rotate)
+// warpgroup 0: warp 0 TMA (Q; K / V in slab mode), warp 1 MMA, warps 2 / 3 paged K / V TMA
+// issuers; warpgroups 1 / 2: softmax of Q0 / Q1; warpgroup 3: paged K rotation in smem
 constexpr int kThreads = 512;
-constexpr int kKLoadThreads = 128, kVLoadThreads = 64;
+constexpr int kKLoadThreads = 128;
 #ifndef TKV_ATTN_KSTAGES
 #define TKV_ATTN_KSTAGES 3  // three K slots: the paged-K loader rotates tile g-1 while tile g lands
 #endif
@@ -58,9 +58,10 @@ constexpr int kKVTile = 2 * kKVHalf;       // 32 KB
 // smem: Q0 Q1 | K ring | V ring | barriers
 constexpr int kQOff = 0, kK0 = 2 * kQTile, kV0 = kK0 + kKStages * kKVTile;
 constexpr int kBarOff = kV0 + kVStages * kKVTile;
-// QFULL[2] QEMPTY[2] KFULL[2] KEMPTY[2] VFULL[2] VEMPTY[2] then per stream: SFULL PFULL PVDONE OFREE
+// QFULL[2] QEMPTY[2] KFULL[K] KEMPTY[K] VFULL[V] VEMPTY[V], per stream: SFULL PFULL PVDONE OFREE,
+// then KLAND[K] (paged: raw K rows landed, before the in-place rotation publishes KFULL)
 constexpr int kStreamBars = 4;
-constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars;
+constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars + kKStages;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
 static_assert(kSmem <= 227 * 1024, "attention smem over the per-CTA limit");
 // TMEM columns: S_s (f32, P_s as packed bf16 over its first 64 columns) at 128 s, O_s at 256 + 128 s
@@ -228,10 +229,10 @@ __host__ __device__ constexpr uint32_t idesc(bool b_mn, int n) {
 }
 
 
-// Walks the window's table segments along increasing prefix rows: the page address of one head's
-// 256-byte row of a cached table image ([K: L][T][kv_dim] then [V: L][T][kv_dim], table_kv.hpp:45-48)
-// for layer slot `ls` (l for K, L + l for V). Rows only grow along a CTA's walk through an item, so
-// each lookup advances the cursor instead of searching (one binary search per item).
+// Walks the window's table segments along increasing prefix rows: the pool row of a cached table
+// image row ([K: L][T][kv_dim] then [V: L][T][kv_dim], table_kv.hpp:45-48) for layer slot `ls`
+// (l for K, L + l for V). Rows only grow along a lane's walk through an item, so each lookup
+// advances the cursor instead of searching (one binary search per item).
 struct SegCursor {
     int seg, next_row0;  // current segment; first row of the next one (INT_MAX past the end)
     GatherSeg sg;
@@ -245,16 +246,24 @@ struct SegCursor {
         sg = a.segs[lo];
         next_row0 = lo + 1 < a.n_segs ? a.segs[lo + 1].out_row0 : 0x7fffffff;
     }
-    __device__ __forceinline__ const uint8_t* row(const AttnArgs& a, int vr, int ls, int kvh) {
+    __device__ __forceinline__ void advance(const AttnArgs& a, int vr) {
         while (vr >= next_row0) {
             ++seg;
             sg = a.segs[seg];
             next_row0 = seg + 1 < a.n_segs ? a.segs[seg + 1].out_row0 : 0x7fffffff;
         }
-        const long row_bytes = long(a.kv_heads) * 128 * 2;
-        const long off = (long(ls) * sg.tokens + (vr - sg.out_row0)) * row_bytes + long(kvh) * 128 * 2;
-        return a.vpool + (long(__ldg(a.page_ids + sg.page_off + (off >> a.page_shift))) << a.page_shift) +
-               (off & ((1L << a.page_shift) - 1));
+    }
+    // the pool row (pool viewed as [page_bytes / row_bytes rows per page]) holding window row vr
+    __device__ __forceinline__ long pool_row(const AttnArgs& a, int vr, int ls) {
+        advance(a, vr);
+        const long off = long(ls) * sg.tokens + (vr - sg.out_row0);  // in rows of the table image
+        const long rpp = 1L << a.rows_shift;                        // rows per page
+        return (long(__ldg(a.page_ids + sg.page_off + (off >> a.rows_shift))) << a.rows_shift) + (off & (rpp - 1));
+    }
+    // rows vr..vr+7 are consecutive pool rows: one segment and one page (after pool_row(vr))
+    __device__ __forceinline__ bool run8(const AttnArgs& a, int vr, int ls) const {
+        const long off = long(ls) * sg.tokens + (vr - sg.out_row0);
+        return vr + 8 <= next_row0 && vr - sg.out_row0 + 8 <= sg.tokens && ((off & ((1L << a.rows_shift) - 1)) + 8) <= (1L << a.rows_shift);
     }
 };
 
@@ -302,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto b_pfull = [&](int st) { return bar(kSB + st * kStreamBars + 1); };
     auto b_pvdone = [&](int st) { return bar(kSB + st * kStreamBars + 2); };
     auto b_ofree = [&](int st) { return bar(kSB + st * kStreamBars + 3); };
+    auto b_kland = [&](int i) { return bar(kSB + 2 * kStreamBars + i); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + kNumBars * 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -319,12 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_pvdone(st), 1);
             mbar_init(b_ofree(st), 4);
         }
-        // K tiles: 1 arrival (TMA lane) or, with paged K, all of warpgroup 3 (own-row tiles: one
-        // thread arms the TMA transaction, the rest arrive plainly)
-        for (int i = 0; i < kKStages; ++i) mbar_init(b_kfull(i), a.kpaged ? kKLoadThreads : 1), mbar_init(b_kempty(i), 1);
-        // V tiles come from the TMA lane (1 arrival) or, with paged V, from warps 2-3 (64 arrivals;
-        // for own-row tiles one of them arms the TMA transaction and the rest arrive plainly)
-        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), a.vpool ? kVLoadThreads : 1), mbar_init(b_vempty(i), 1);
+        // slab mode: K / V tiles from the TMA lanes (1 arrival each). Paged mode: raw K rows land on
+        // KLAND (the K issuer warp arms it), warpgroup 3 rotates them and all 128 threads arrive on
+        // KFULL; V tiles land on VFULL armed by the V issuer warp.
+        for (int i = 0; i < kKStages; ++i)
+            mbar_init(b_kfull(i), a.kpaged ? kKLoadThreads : 1), mbar_init(b_kempty(i), 1), mbar_init(b_kland(i), 1);
+        for (int i = 0; i < kVStages; ++i) mbar_init(b_vfull(i), 1), mbar_init(b_vempty(i), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -374,14 +384,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                it.sq.q_row0 + it.tok0 + st * TQ);
                 }
                 TR(8, j);
-                if (a.kpaged) continue;  // K tiles come from warpgroup 3
+                if (a.kpaged) continue;  // paged mode: K tiles come from the K issuer warp
                 auto prefetch_kv = [&](int t) {  // K always; V here only when it comes by TMA
                     bool ctx;
                     const int row = tile_row(it, t, ctx);
                     for (int h = 0; h < 2; ++h) {
                         const bool hm = ctx && a.k_hm_rows;
                         tma_prefetch_2d(ctx ? &mk_ctx : &mk_own, hm ? h * 64 : it.kvh * D + h * 64, hm ? int(it.kvh * a.k_hm_rows) + row : row);
-                        if (!a.vpool || !ctx) tma_prefetch_2d(ctx ? &mv_ctx : &mv_own, it.kvh * D + h * 64, row);
+                        tma_prefetch_2d(ctx ? &mv_ctx : &mv_own, it.kvh * D + h * 64, row);
                     }
                 };
                 const int pf = a.prefetch;
@@ -401,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                hm ? int(it.kvh * a.k_hm_rows) + row : row);
                 }
             }
-        } else if (lane == 16 && !a.vpool) {  // ---- TMA: V tiles
+        } else if (lane == 16 && !a.kpaged) {  // ---- TMA: V tiles (slab mode)
             long g = 0;
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
                 const Item it = item(w);
@@ -417,48 +427,68 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if ((warp == 2 || warp == 3) && a.vpool) {
-        // ---- paged V: cached-prefix tiles copied from the table pages with 16-byte cp.async into
-        // the swizzled tile; 16 threads per 256-byte head row (two whole rows per warp instruction,
-        // every L2 sector fetched once), own-row tiles by TMA
-        const int tid = threadIdx.x - 64;
-        const int c = tid & 15, sub = tid >> 4;  // chunk of the head row, row phase (rows sub + 4i)
+    } else if ((warp == 2 || warp == 3) && a.kpaged) {
+        // ---- paged issuers: warp 2 the K tiles (onto KLAND), warp 3 the V tiles (onto VFULL).
+        // Cached-prefix tiles come straight from the tables' pool pages by TMA over the pool viewed
+        // as [pool rows][kv_heads * 128] (mk_ctx: 8-row boxes, mv_ctx: 1-row boxes, 128-byte
+        // swizzle): lane j < 16 owns rows [8j, 8j + 8) of the tile; when those 8 rows are one run of
+        // one table segment inside one page they move as one 8-row box per 64-column half, else row
+        // by row. Own-row tiles (rotated by the QKV epilogue) by TMA from the own-row buffers.
+        const bool is_k = warp == 2;
+        const int ls = is_k ? a.layer : a.layers + a.layer;  // layer slot of the table image
         SegCursor cur;
         long g = 0;
         for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
             const Item it = item(w);
-            if (it.n_ctx_tiles) cur.seek(a, it.sq.ctx_row0);
+            if (it.n_ctx_tiles && lane < 16) cur.seek(a, it.sq.ctx_row0 + min(8 * lane, it.sq.n_ctx - 1));
             for (int t = 0; t < it.n_tiles; ++t, ++g) {
-                const int sv = int(g % kVStages);
-                mbar_wait(b_vempty(sv), int((g / kVStages) & 1) ^ 1);
-                if (tid == 0) TR(1, g);
+                const int stg = int(g % (is_k ? kKStages : kVStages));
+                const long lap = g / (is_k ? kKStages : kVStages);
+                mbar_wait(is_k ? b_kempty(stg) : b_vempty(stg), int(lap & 1) ^ 1);
+                if (lane == 0) TR(is_k ? 0 : 1, g);
                 bool ctx;
                 const int row = tile_row(it, t, ctx);
-                const uint32_t dv = s0 + kV0 + sv * kKVTile;
+                const uint32_t dst = s0 + (is_k ? kK0 : kV0) + stg * kKVTile;
+                const uint32_t fb = is_k ? b_kland(stg) : b_vfull(stg);
                 if (!ctx) {
-                    if (tid == 0) {
-                        mbar_expect_tx(b_vfull(sv), kKVTile);
-                        for (int h = 0; h < 2; ++h) tma_2d(dv + h * kKVHalf, &mv_own, b_vfull(sv), it.kvh * D + h * 64, row);
-                    } else {
-                        mbar_arrive(b_vfull(sv));
+                    if (lane == 0) {
+                        mbar_expect_tx(fb, kKVTile);
+                        for (int h = 0; h < 2; ++h) tma_2d(dst + h * kKVHalf, is_k ? &mk_own : &mv_own, fb, it.kvh * D + h * 64, row);
                     }
                     continue;
                 }
-                bool zeros = false;
-                for (int rr = sub; rr < BN; rr += kVLoadThreads / 16) {
-                    const int key = t * BN + rr;  // key index within this sequence's prefix
-                    const uint32_t dst = dv + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-                    if (key < it.sq.n_ctx) {
-                        const uint8_t* src = cur.row(a, it.sq.ctx_row0 + key, a.layers + a.layer, it.kvh) + c * 16;
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-                    } else {  // past the prefix: finite zeros (masked in the softmax)
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
-                        zeros = true;
+                const int key0 = t * BN + 8 * lane;
+                const int nv = lane < 16 ? max(0, min(8, it.sq.n_ctx - key0)) : 0;
+                if (!is_k && t * BN + BN > it.sq.n_ctx) {  // V rows past the prefix: finite zeros (P is 0 there)
+                    for (int i = lane; i < (t * BN + BN - it.sq.n_ctx) * 16; i += 32) {
+                        const int rr = it.sq.n_ctx - t * BN + (i >> 4), c = i & 15;
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst + (c >> 3) * kKVHalf + rr * 128 +
+                                                                             (((c & 7) ^ (rr & 7)) << 4)),
+                                     "r"(0u)
+                                     : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                uint32_t bytes = uint32_t(nv) * D * 2;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+                __syncwarp();
+                if (lane == 0) mbar_expect_tx(fb, bytes);
+                __syncwarp();
+                if (nv > 0) {
+                    const int vr = it.sq.ctx_row0 + key0;
+                    const long pr = cur.pool_row(a, vr, ls);
+                    if (nv == 8 && cur.run8(a, vr, ls)) {
+                        for (int h = 0; h < 2; ++h)
+                            tma_2d(dst + h * kKVHalf + 8 * lane * 128, &mk_ctx, fb, it.kvh * D + h * 64, int(pr));
+                    } else {
+                        for (int r = 0; r < nv; ++r) {
+                            const long p1 = r == 0 ? pr : cur.pool_row(a, vr + r, ls);
+                            for (int h = 0; h < 2; ++h)
+                                tma_2d(dst + h * kKVHalf + (8 * lane + r) * 128, &mv_ctx, fb, it.kvh * D + h * 64, int(p1));
+                        }
                     }
                 }
-                if (zeros) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(b_vfull(sv)) : "memory");
-                if (tid == 0) TR(15, g);
             }
         }
     } else if (warp == 1) {
@@ -487,7 +517,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (st == 0) {
                     mbar_wait(b_kfull(sk), int((c.gi / kKStages) & 1));
                     TR(2, c.gi);
-                    if (a.kpaged) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // rotated rows -> tensor core
                 }
                 if (c.t == 0) mbar_wait(b_qfull(st), c.j & 1);
                 fence_after();
@@ -505,7 +534,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (st == 0) {
                     mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
                     TR(11, c.gi);
-                    if (a.vpool) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async rows -> tensor core
                 }
                 mbar_wait(b_pfull(st), int(c.gi & 1));
                 if (st == 0) TR(4, c.gi);
@@ -542,16 +570,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 12) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         if (a.kpaged) {
-            // ---- paged K: raw rows by 16-byte cp.async into the swizzled ring slot (16 threads per
-            // 256-byte head row), then each thread rotates the chunks it loaded in place: interleaved
-            // pairs k = 4c..4c+3 at the key's prefix position p (assemble, attention.hpp:300-362),
-            // a' = a cos - b sin, b' = a sin + b cos in f32 and rounded to bf16 (the gather's formula).
-            // cos/sin of p come from the f32 table at the thread's first row of the tile and advance
-            // by R(8 theta_k) per row step (8 rows apart): no table traffic per row. One tile of
-            // lookahead: tile g's loads are issued before tile g-1 is rotated and published.
+            // ---- paged K rotation: once a tile's raw rows have landed (KLAND), every thread rotates
+            // its chunks in place — interleaved pairs k = 4c..4c+3 of its rows at their prefix
+            // positions p (assemble, attention.hpp:300-362): a' = a cos - b sin, b' = a sin + b cos in
+            // f32, rounded to bf16 (the gather's formula) — writes zeros into rows past the prefix,
+            // and publishes the tile on KFULL. cos/sin of p come from the f32 table at the thread's
+            // first row and advance by R(2 theta_k) per row step (its rows are 2 apart).
             const int kt = threadIdx.x - 384;
-            const int c = kt & 15, sub = kt >> 4;  // chunk of the head row, row phase (rows sub + 8i)
-            constexpr int kRowStep = kKLoadThreads / 16;
+            const int kw = kt >> 5;                   // warp kw owns tile rows [32 kw, 32 kw + 32)
+            const int c = lane & 15, hl = lane >> 4;  // chunk of the head row; rows 32 kw + 2i + hl
+            constexpr int kRowStep = 2;
             const int half = D / 2;
             float cd[4], sd[4];  // R(kRowStep theta_k), k = 4c..4c+3
             {
@@ -560,78 +588,60 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cd[0] = x.x, cd[1] = x.y, cd[2] = x.z, cd[3] = x.w;
                 sd[0] = y.x, sd[1] = y.y, sd[2] = y.z, sd[3] = y.w;
             }
-            SegCursor cur;
-            struct Pend {
-                int slot, tile, n_ctx;  // tile < 0: nothing to rotate
-            } pend{0, -1, 0};
-            auto finish = [&](const Pend& p) {  // rotate a landed ctx tile in place and publish it
-                if (p.tile < 0) return;
-                const uint32_t dk = s0 + kK0 + p.slot * kKVTile;
-                const int pos0 = p.tile * BN + sub;
-                if (pos0 < p.n_ctx) {
-                    float cs[4], sn[4];
-                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + long(pos0) * half + 4 * c));
-                    const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + long(pos0) * half + 4 * c));
-                    cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
-                    sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
-                    for (int rr = sub; rr < BN && p.tile * BN + rr < p.n_ctx; rr += kRowStep) {
-                        const uint32_t at = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-                        uint32_t w[4];
-                        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(at));
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const float x0 = __uint_as_float(w[j] << 16), x1 = __uint_as_float(w[j] & 0xffff0000u);
-                            w[j] = pack_bf16x2(fmaf(x0, cs[j], -x1 * sn[j]), fmaf(x0, sn[j], x1 * cs[j]));
-                            const float cn = fmaf(cs[j], cd[j], -sn[j] * sd[j]);
-                            sn[j] = fmaf(sn[j], cd[j], cs[j] * sd[j]);
-                            cs[j] = cn;
-                        }
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
-                                     : "memory");
-                    }
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(b_kfull(p.slot));
-            };
             long g = 0;
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
                 const Item it = item(w);
-                if (it.n_ctx_tiles) cur.seek(a, it.sq.ctx_row0);
                 for (int t = 0; t < it.n_tiles; ++t, ++g) {
                     const int sk = int(g % kKStages);
-                    mbar_wait(b_kempty(sk), int((g / kKStages) & 1) ^ 1);
-                    if (kt == 0) TR(0, g);
-                    bool ctx;
-                    const int row = tile_row(it, t, ctx);
-                    const uint32_t dk = s0 + kK0 + sk * kKVTile;
-                    if (!ctx) {  // own rows: rotated by the QKV epilogue, one TMA transaction
-                        if (kt == 0) {
-                            mbar_expect_tx(b_kfull(sk), kKVTile);
-                            for (int h = 0; h < 2; ++h) tma_2d(dk + h * kKVHalf, &mk_own, b_kfull(sk), it.kvh * D + h * 64, row);
-                        } else {
-                            mbar_arrive(b_kfull(sk));
+                    mbar_wait(b_kland(sk), int((g / kKStages) & 1));
+                    if (t < it.n_ctx_tiles) {
+                        const uint32_t dk = s0 + kK0 + sk * kKVTile;
+                        const int pos0 = t * BN + 32 * kw + hl;
+                        float cs[4], sn[4];
+                        if (pos0 < it.sq.n_ctx) {
+                            const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + long(pos0) * half + 4 * c));
+                            const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + long(pos0) * half + 4 * c));
+                            cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
+                            sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
                         }
-                    } else {
-                        for (int rr = sub; rr < BN; rr += kRowStep) {
-                            const int key = t * BN + rr;
-                            const uint32_t dst = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
-                            if (key < it.sq.n_ctx) {
-                                const uint8_t* src = cur.row(a, it.sq.ctx_row0 + key, a.layer, it.kvh) + c * 16;
-                                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-                            } else {
-                                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst), "r"(0u) : "memory");
+#pragma unroll 4
+                        for (int i = 0; i < 16; ++i) {
+                            const int rr = 32 * kw + 2 * i + hl;
+                            const uint32_t at = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                            uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                            if (pos0 + 2 * i < it.sq.n_ctx) {
+                                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                             : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
+                                             : "r"(at));
+#ifdef TKV_KROT_TABLE  // A/B knob: cos/sin of every row from the f32 table (bit-exact with the gather)
+                                {
+                                    const long pp = long(pos0 + 2 * i) * half + 4 * c;
+                                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + pp));
+                                    const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + pp));
+                                    cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
+                                    sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
+                                }
+#endif
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float x0 = __uint_as_float(wv[j] << 16), x1 = __uint_as_float(wv[j] & 0xffff0000u);
+                                    wv[j] = pack_bf16x2(fmaf(x0, cs[j], -x1 * sn[j]), fmaf(x0, sn[j], x1 * cs[j]));
+#ifndef TKV_KROT_TABLE
+                                    const float cn = fmaf(cs[j], cd[j], -sn[j] * sd[j]);
+                                    sn[j] = fmaf(sn[j], cd[j], cs[j] * sd[j]);
+                                    cs[j] = cn;
+#endif
+                                }
                             }
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
+                                         : "memory");
                         }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     }
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                    asm volatile("cp.async.wait_group 1;" ::: "memory");  // the previous tile's rows have landed
-                    finish(pend);
-                    if (kt == 0 && g > 0) TR(9, g - 1);
-                    pend = ctx ? Pend{sk, t, it.sq.n_ctx} : Pend{0, -1, 0};
+                    mbar_arrive(b_kfull(sk));
+                    if (kt == 0) TR(9, g);
                 }
             }
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            finish(pend);
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
@@ -826,12 +836,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// [rows][cols] bf16 (cols contiguous), box = 64 cols x 128 rows, 128-byte swizzle
-CUtensorMap rows_map(const void* base, long rows, int cols) {
+// [rows][cols] bf16 (cols contiguous), box = 64 cols x box_rows rows, 128-byte swizzle
+CUtensorMap rows_map(const void* base, long rows, int cols, int box_rows = BN) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(std::max(1L, rows))};
     const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
-    const cuuint32_t box[2] = {64, cuuint32_t(BN)}, es[2] = {1, 1};  // 64 cols x BN rows
+    const cuuint32_t box[2] = {64, cuuint32_t(box_rows)}, es[2] = {1, 1};  // 64 cols x box_rows rows
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -867,8 +877,10 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
     if (a.mode == 1 && !a.row_lo) throw std::invalid_argument("tcgen05 block-mask attention needs per-row group starts");
     ensure_smem_optin(reinterpret_cast<const void*>(attn_tc5_kernel), kSmem);
     const int kvd = a.kv_heads * D;
-    const CUtensorMap mkc = a.k_hm_rows ? rows_map(a.k_ctx, a.k_hm_rows * a.kv_heads, D) : rows_map(a.k_ctx, ctx_rows, kvd);
-    const CUtensorMap mvc = rows_map(a.v_ctx, ctx_rows, kvd);
+    // paged mode: the pool as [pool rows][kv_dim] — 8-row boxes (mkc) and single-row boxes (mvc)
+    const CUtensorMap mkc = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 8)
+                            : a.k_hm_rows ? rows_map(a.k_ctx, a.k_hm_rows * a.kv_heads, D) : rows_map(a.k_ctx, ctx_rows, kvd);
+    const CUtensorMap mvc = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 1) : rows_map(a.v_ctx, ctx_rows, kvd);
     const CUtensorMap mko = rows_map(a.k_own, own_rows, kvd), mvo = rows_map(a.v_own, own_rows, kvd);
     const CUtensorMap mq = q_map(a.q, own_rows, a.num_heads, a.num_heads / a.kv_heads);
     static const char* trace_path = std::getenv("TKV_ATTN_TRACE");

@@ -143,7 +143,29 @@ __device__ __forceinline__ void rope32(float* v, int col0, int head_dim, int pos
 
 __device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
 
-__device__ void epilogue32(const EpiParams& ep, int m, int n0, float* v) {
+// norm-fold consumer: the row's RMS scale from the producer's partials (1 when not folded)
+__device__ __forceinline__ float ep_row_scale(const EpiParams& ep, int m, int M) {
+    if (!ep.ss_in || m >= M) return 1.f;
+    const float4* p = reinterpret_cast<const float4*>(ep.ss_in + long(m) * ep.ss_chunks);
+    float acc = 0.f;
+    for (int i = 0; i < ep.ss_chunks / 4; ++i) {
+        const float4 x = __ldg(p + i);
+        acc += (x.x + x.y) + (x.z + x.w);
+    }
+    return rsqrtf(acc / ep.ss_n + ep.eps);
+}
+// norm-fold producer: one 128-column partial of the row's sum of squares
+__device__ __forceinline__ void ep_store_ssq(const EpiParams& ep, int m, int M, int n_end, float& ssq) {
+    if (ep.ss_out && m < M) ep.ss_out[long(m) * (ep.ldo / kNormChunk) + (n_end - 1) / kNormChunk] = ssq;
+    ssq = 0.f;
+}
+
+// returns the sum of squares of the updated residual values (resid_f32 with xb_out), else 0
+__device__ float epilogue32(const EpiParams& ep, int m, int n0, float* v, float rs = 1.f) {
+    if (rs != 1.f) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= rs;
+    }
     switch (ep.kind) {
         case Epi::store_bf16:
             store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + long(m) * ep.ldo + n0, v);
@@ -161,6 +183,14 @@ __device__ void epilogue32(const EpiParams& ep, int m, int n0, float* v) {
                 float4 r = d[i];
                 r.x += v[4 * i], r.y += v[4 * i + 1], r.z += v[4 * i + 2], r.w += v[4 * i + 3];
                 d[i] = r;
+                v[4 * i] = r.x, v[4 * i + 1] = r.y, v[4 * i + 2] = r.z, v[4 * i + 3] = r.w;
+            }
+            if (ep.xb_out) {
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.xb_out) + long(m) * ep.ldo + n0, v);
+                float s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < 32; ++i) s2[i & 3] = fmaf(v[i], v[i], s2[i & 3]);
+                return (s2[0] + s2[1]) + (s2[2] + s2[3]);
             }
             break;
         }
@@ -197,6 +227,7 @@ __device__ void epilogue32(const EpiParams& ep, int m, int n0, float* v) {
             break;
         }
     }
+    return 0.f;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -278,10 +309,13 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     const int m = m0 + warp * 32 + lane;
+    const float rs = ep_row_scale(ep, m, M);
+    float ssq = 0.f;
     for (int c = 0; c < BN; c += 32) {
         float v[32];
         tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c, v);
-        if (m < M && n0 + c < N) epilogue32(ep, m, n0 + c, v);
+        if (m < M && n0 + c < N) ssq += epilogue32(ep, m, n0 + c, v, rs);
+        if (((c + 32) % kNormChunk) == 0) ep_store_ssq(ep, m, M, n0 + c + 32, ssq);
     }
     tc_fence_before();
     __syncthreads();
@@ -395,10 +429,13 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
             mbar_wait(tfull0 + 8 * acc, (local >> 1) & 1);
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
+            const float rs = ep_row_scale(ep, m, M);
+            float ssq = 0.f;
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
                 tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
-                if (m < M && n0 + c < N) epilogue32(ep, m, n0 + c, v);
+                if (m < M && n0 + c < N) ssq += epilogue32(ep, m, n0 + c, v, rs);
+                if (((c + 32) % kNormChunk) == 0) ep_store_ssq(ep, m, M, n0 + c + 32, ssq);
             }
             tc_fence_before();
             __syncwarp();
@@ -538,10 +575,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
             mbar_wait_b(tfull0 + 8 * acc, (local >> 1) & 1);
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
+            const float rs = ep_row_scale(ep, m, M);
+            float ssq = 0.f;
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
                 tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
-                if (m < M) epilogue32(ep, m, n0 + c, v);
+                if (m < M) ssq += epilogue32(ep, m, n0 + c, v, rs);
+                if (((c + 32) % kNormChunk) == 0) ep_store_ssq(ep, m, M, n0 + c + 32, ssq);
             }
             tc_fence_before();
             __syncwarp();
@@ -683,10 +723,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
             mbar_wait_b(tfull0 + 8 * acc, (local >> 1) & 1);
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
+            const float rs = ep_row_scale(ep, m, M);
+            float ssq = 0.f;
             for (int c = 0; c < BN; c += 32) {
                 float v[32];
                 tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
-                if (m < M) epilogue32(ep, m, n0 + c, v);
+                if (m < M) ssq += epilogue32(ep, m, n0 + c, v, rs);
+                if (((c + 32) % kNormChunk) == 0) ep_store_ssq(ep, m, M, n0 + c + 32, ssq);
             }
             tc_fence_before();
             __syncwarp();
@@ -807,6 +850,8 @@ int gemm_mode() {  // TKV_GEMM = single | pair | 2sm (A/B measurements); default
 void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     if (M == 0) return;
     if (K % 8 || N % 32) throw std::invalid_argument("gemm_bf16: need K % 8 == 0 and N % 32 == 0");
+    if ((ep.ss_out && (N % kNormChunk || ep.ldo != N)) || (ep.ss_in && ep.ss_chunks % 4))
+        throw std::invalid_argument("gemm_bf16: folded norm needs 128-column partials");
     // persistent warp-specialised kernel; 128x256 tiles when N allows, else 128x128 with a deeper ring
     if (N % 256 == 0 && M > 128 && gemm_mode() == 2)
         launch_2sm<6>(A, B, M, N, K, ep, s);
@@ -831,6 +876,7 @@ void gemm_bf16_classic(const void* A, const void* B, int M, int N, int K, const 
 
 void gemm_bf16_simt(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s) {
     if (M == 0) return;
+    if (ep.ss_in || ep.ss_out) throw std::invalid_argument("gemm_bf16_simt: no folded-norm epilogue");
     const long n = long(M) * (N / 32);
     gemm_simt_kernel<<<ceil_div(n, 128), 128, 0, s>>>(static_cast<const __nv_bfloat16*>(A),
                                                       static_cast<const __nv_bfloat16*>(B), M, N, K, ep);

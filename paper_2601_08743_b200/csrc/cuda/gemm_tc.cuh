@@ -30,7 +30,19 @@ struct EpiParams {
     const int32_t* pos = nullptr;        // [M] global positions
     const float* cos_f = nullptr;        // [max_pos][head_dim/2]
     const float* sin_f = nullptr;
+    // RMSNorm folded into the GEMMs (no norm kernel between a residual update and the next
+    // projection). Producer (resid_f32): xb_out[m][n] = bf16(updated residual) and ss_out[m][n / 128]
+    // = sum of squares of its 128-column chunk, written by the one thread that owns that row of
+    // the tile (no atomics: fixed order, deterministic). Consumer: the A operand is that bf16(x);
+    // every accumulator row is scaled by rsqrt(sum_c ss_in[m][c] / ss_n + eps) before the epilogue
+    // op, i.e. norm(x) . W = rs(x) * (x . W) with the rounding of x instead of norm(x).
+    void* xb_out = nullptr;        // [M][ldo] bf16
+    float* ss_out = nullptr;       // [M][ldo / 128]
+    const float* ss_in = nullptr;  // [M][ss_chunks]
+    int ss_chunks = 0;
+    float ss_n = 1.f, eps = 0.f;
 };
+constexpr int kNormChunk = 128;  // columns per sum-of-squares partial
 
 // Launch on stream; A, B device pointers (bf16 bits), K % 8 == 0, N % 32 == 0.
 void gemm_bf16(const void* A, const void* B, int M, int N, int K, const EpiParams& ep, cudaStream_t s);

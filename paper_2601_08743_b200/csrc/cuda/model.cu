@@ -187,7 +187,9 @@ void Model::ensure_ws(int M, cudaStream_t s) {
     const size_t es = dtype_size(c.dtype);
     const long h = c.hidden(), qd = long(c.num_heads) * c.head_dim, kvd = c.kv_dim(), f = c.ffn;
     // x (f32 or T), xn, q, k, v, attn, proj (T), mid (f), gate (f)
-    const size_t per_row = size_t(h) * std::max<size_t>(4, es) + (h + qd + 2 * kvd + qd + h) * es + 2 * size_t(f) * es + 64;
+    // + the folded norm's sum-of-squares partials (h / 128 floats)
+    const size_t per_row = size_t(h) * std::max<size_t>(4, es) + (h + qd + 2 * kvd + qd + h) * es + 2 * size_t(f) * es + 64 +
+                           size_t(h / 128 + 4) * 4;
     TKV_CUDA_CHECK(cudaMalloc(&ws_, per_row * cap + 4096));
     TKV_CUDA_CHECK(cudaMemsetAsync(ws_, 0, per_row * cap + 4096, s));  // finite padding rows for masked tiles
     ws_rows_ = cap;
@@ -247,6 +249,27 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
     void* v = take(size_t(R) * kvd * 2);
     void* att = take(size_t(R) * qd * 2);
     void* mid = take(size_t(R) * f * 2);
+    float* ssq = static_cast<float*>(take(size_t(R) * (h / 128 + 4) * 4));
+    // RMSNorm folded into the GEMMs (gemm_tc.cuh EpiParams): the O / down projections' epilogues
+    // write bf16(x) into xn plus per-128-column sums of squares, the next projection scales its
+    // accumulator rows; no norm kernel inside the layer stack. TKV_NORM_FOLD=0: separate norms.
+    static const bool fold_env = [] {
+        const char* e = std::getenv("TKV_NORM_FOLD");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool fold = fold_env && rms && h % 512 == 0;
+    auto fold_in = [&](EpiParams& e, bool on) {
+        if (!on) return;
+        e.ss_in = ssq;
+        e.ss_chunks = h / 128;
+        e.ss_n = float(h);
+        e.eps = eps;
+    };
+    auto fold_out = [&](EpiParams& e, bool on) {
+        if (!on) return;
+        e.xb_out = xn;
+        e.ss_out = ssq;
+    };
 
     // attention work list: (seq, first token, kv head)
     // tcgen05 attention over cached prefixes at head_dim 128 (the Llama-shaped serving path); the
@@ -279,18 +302,15 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         if (contiguous) d_row_lo = static_cast<const int32_t*>(ring_.upload(lo.data(), lo.size() * 4, s));
     }
     const bool use_tc5 = attn_impl_ == 0 && c.head_dim == 128 && 128 % G == 0 && (a.mode == 0 || d_row_lo != nullptr);
-    // paged V needs the tcgen05 kernel, the bf16 TMA gather (K only) and power-of-two pages
-    const bool paged_v = a.paged_v && use_tc5 && a.mode == 0 && a.gather_segs && a.gather_chunks &&
-                         a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1));
-    // with paged V the K slab is written head-major (one kv head's key tile = one contiguous block)
-    static const bool hm_env = [] {
-        const char* e = std::getenv("TKV_K_HEAD_MAJOR");
-        return !(e && std::atoi(e) == 0);
-    }();
-    // paged K: the attention's loader warps read K from the pages too and rotate it in smem, so
-    // no gather runs and no K slab is written or re-read
-    const bool paged_k = paged_v && a.paged_k;
-    const bool k_head_major = paged_v && !paged_k && hm_env && gather_use_tma();
+    // paged prefix (the serving default): the tcgen05 attention reads cached K and V straight from
+    // the pool pages by TMA and rotates K in shared memory — no gather, no prefix slab. Needs bf16
+    // images and power-of-two pages holding whole token rows; else (or TKV_PAGED_K / TKV_PAGED_V =
+    // 0) the gather writes rotated K and V into the one-layer slab first.
+    const size_t kv_row_bytes = size_t(kvd) * 2;
+    auto pow2 = [](size_t v) { return v && !(v & (v - 1)); };
+    const bool paged = a.paged_v && a.paged_k && use_tc5 && a.mode == 0 && a.gather_segs && a.gather_in == DType::bf16 &&
+                       a.gather_pool_bytes > 0 && pow2(a.gather_page_bytes) && pow2(kv_row_bytes) &&
+                       a.gather_page_bytes % kv_row_bytes == 0;
     const int tq = use_tc5 ? attn_tc5_rows_per_tile(c.num_heads, c.kv_heads) : attn_rows_per_tile(c.num_heads, c.kv_heads);
     std::vector<int4> tiles;
     for (int si = 0; si < a.n_seqs; ++si)
@@ -338,6 +358,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         e.pos = a.pos;
         e.cos_f = rope_.cos_f();
         e.sin_f = rope_.sin_f();
+        fold_in(e, fold && l > 0);  // layer 0 reads the embedding's normalised rows
         run_gemm(xn, L.wqkv, M, qd + 2 * kvd, h, e);
 
         AttnArgs aa;
@@ -345,7 +366,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.k_own = static_cast<const __nv_bfloat16*>(k);
         aa.v_own = static_cast<const __nv_bfloat16*>(v_l);
         const bool streamed = a.gather_segs != nullptr;
-        if (streamed && !paged_k) {
+        if (streamed && !paged) {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing_) {
                 e0 = timing_event();
@@ -355,8 +376,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             if (a.gather_chunks && a.gather_in == DType::bf16 && !(a.gather_page_bytes & (a.gather_page_bytes - 1)))
                 launch_gather_rope_bf16(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_chunks,
                                         a.gather_n_chunks, c.num_layers, l, kvd, c.head_dim, rope_.cos_f(), rope_.sin_f(),
-                                        const_cast<void*>(a.ctx_k), paged_v ? nullptr : const_cast<void*>(a.ctx_v),
-                                        a.ctx_rows, s, k_head_major);
+                                        const_cast<void*>(a.ctx_k), const_cast<void*>(a.ctx_v), a.ctx_rows, s);
             else
                 launch_gather_rope(a.gather_pool, a.gather_page_bytes, a.gather_pages, a.gather_segs, a.gather_n_segs,
                                    a.gather_rows, c.num_layers, kvd, c.head_dim, a.gather_in, DType::bf16, rope_.cos_d(),
@@ -365,9 +385,9 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             ++nl;
             if (timing_) {
                 TKV_CUDA_CHECK(cudaEventRecord(e1, s));
-                // algorithmic bytes: each prefix row's K (and V unless paged) read from the pages + written
+                // algorithmic bytes: each prefix row's K and V read from the pages + written
                 const double in_b = a.gather_in == DType::bf16 ? 2.0 : 4.0;
-                add_timed(e0, e1, -double(a.ctx_rows) * kvd * (paged_v ? 1 : 2) * (in_b + 2.0));
+                add_timed(e0, e1, -double(a.ctx_rows) * kvd * 2 * (in_b + 2.0));
             }
         }
         const size_t ctx_off = streamed ? 0 : size_t(l) * a.ctx_rows * kvd * 2;
@@ -388,18 +408,18 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             return e ? std::atoi(e) : 0;
         }();
         aa.prefetch = attn_prefetch;
-        if (k_head_major) aa.k_hm_rows = a.ctx_rows;
-        if (paged_v) {
+        if (paged) {
             aa.vpool = a.gather_pool;
+            aa.pool_rows = long(a.gather_pool_bytes / kv_row_bytes);
             int sh = 0;
-            while ((size_t(1) << sh) < a.gather_page_bytes) ++sh;
-            aa.page_shift = sh;
+            while ((kv_row_bytes << sh) < a.gather_page_bytes) ++sh;
+            aa.rows_shift = sh;
             aa.page_ids = a.gather_pages;
             aa.segs = a.gather_segs;
             aa.n_segs = a.gather_n_segs;
             aa.layer = l;
             aa.layers = c.num_layers;
-            aa.kpaged = paged_k;
+            aa.kpaged = true;
             aa.cos_f = rope_.cos_f();
             aa.sin_f = rope_.sin_f();
         }
@@ -427,12 +447,17 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         eo.kind = Epi::resid_f32;
         eo.out = x;
         eo.ldo = h;
+        fold_out(eo, fold);
         run_gemm(att, L.wo, M, h, qd, eo);
-        norm_bf16(x, nullptr, M, h, xn, rms, eps, s);
+        if (!fold) {
+            norm_bf16(x, nullptr, M, h, xn, rms, eps, s);
+            ++nl;
+        }
 
         EpiParams em;
         em.out = mid;
         em.ldo = f;
+        fold_in(em, fold);
         if (c.mlp == 1) {
             em.kind = Epi::swiglu_bf16;
             run_gemm(xn, L.w_in, M, 2 * f, h, em);
@@ -444,9 +469,10 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         ed.kind = Epi::resid_f32;
         ed.out = x;
         ed.ldo = h;
+        fold_out(ed, fold && l + 1 < c.num_layers);
         run_gemm(mid, L.w_out, M, h, f, ed);
-        nl += 6;
-        if (l + 1 < c.num_layers) {
+        nl += 5;
+        if (l + 1 < c.num_layers && !fold) {
             norm_bf16(x, nullptr, M, h, xn, rms, eps, s);
             ++nl;
         }

@@ -87,8 +87,9 @@ struct FwdArgs {
     const GatherSeg* gather_segs = nullptr; // device
     int gather_n_segs = 0, gather_rows = 0;
     const int4* gather_chunks = nullptr;    // device: {seg, t0, rows, 0} (bf16 fast path)
-    bool paged_v = false;                   // tcgen05 attention reads prefix V from the pages (gather: K only)
-    bool paged_k = false;                   // ... and K too, rotated in shared memory (no gather, no slab)
+    size_t gather_pool_bytes = 0;           // pool extent (paged mode's TMA view of the pool)
+    bool paged_v = false, paged_k = false;  // both: the tcgen05 attention reads the prefix from the
+                                            // pages (K rotated in smem); else the gather fills the slab
     int gather_n_chunks = 0;
     DType gather_in = DType::bf16;
     void* kraw_out = nullptr;           // optional [L][M][kv_dim] pre-rotation keys (offline encode)

@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "common.cuh"
@@ -25,7 +26,7 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxWords = 64;    // tables up to 4096
 constexpr int kMaxCluster = 16;  // non-portable cluster size (opted in below)
@@ -47,6 +48,10 @@ __device__ __forceinline__ unsigned long long warp_min(unsigned long long v) {
     return v;
 }
 
+// W = compile-time bound on the words per row (cur is held in registers); rows in shared memory
+// are word-major ([word][row]) so a warp's 32 lanes read 32 consecutive rows' word w at once
+// (conflict-free, 256 bytes per request); rows left in global memory stay row-major.
+template <int W>
 __global__ void __launch_bounds__(kThreads, 1)
     rerank_cluster_kernel(const uint64_t* __restrict__ g_inc, int n, int words, int first, int per, int rows_in_smem,
                           int32_t* __restrict__ order) {
@@ -57,27 +62,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     Xch* xch = reinterpret_cast<Xch*>(sm);                                                 // [2][kMaxCluster]
     unsigned long long* red = reinterpret_cast<unsigned long long*>(xch + 2 * kMaxCluster);  // [32]
     uint64_t* cur0 = reinterpret_cast<uint64_t*>(red + 32);                                 // [kMaxWords]
-    uint64_t* s_rows = cur0 + kMaxWords;                                                    // [per][words]
+    uint64_t* s_rows = cur0 + kMaxWords;                                                    // [words][per]
     const int r0 = rank * per;
     const int n_loc = max(0, min(n - r0, per));
-    const uint64_t* rows = rows_in_smem ? s_rows : g_inc + long(r0) * words;
     if (rows_in_smem)
-        for (long i = tid; i < long(n_loc) * words; i += kThreads) s_rows[i] = g_inc[long(r0) * words + i];
+        for (long i = tid; i < long(n_loc) * words; i += kThreads) {
+            const long r = i / words, w = i % words;
+            s_rows[w * per + r] = g_inc[long(r0) * words + i];
+        }
     if (tid < words) cur0[tid] = g_inc[long(first) * words + tid];
     // used bits of this thread's rows: bit j <-> local row tid + j * kThreads
     uint32_t used = 0;
     if (first >= r0 && first < r0 + n_loc && (first - r0) % kThreads == tid) used |= 1u << ((first - r0) / kThreads);
     if (rank == 0 && tid == 0) order[0] = first;
-    cl.sync();  // every CTA's exchange area exists before the first remote store
+    cl.sync();  // every CTA's exchange area and rows exist before the first remote store
     const uint64_t* cur = cur0;
     for (int step = 1; step < n; ++step) {
+        uint64_t cw[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) cw[w] = w < words ? cur[w] : 0ull;
         unsigned long long best = ~0ull;
         int j = 0;
         for (int i = tid; i < n_loc; i += kThreads, ++j) {
             if ((used >> j) & 1u) continue;
-            const uint64_t* row = rows + long(i) * words;
             uint32_t d = 0;
-            for (int w = 0; w < words; ++w) d += __popcll(row[w] ^ cur[w]);
+            if (rows_in_smem) {
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    if (w < words) d += __popcll(s_rows[long(w) * per + i] ^ cw[w]);
+            } else {
+                const uint64_t* row = g_inc + long(r0 + i) * words;
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    if (w < words) d += __popcll(__ldg(row + w) ^ cw[w]);
+            }
             const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | uint32_t(r0 + i);
             best = key < best ? key : best;
         }
@@ -89,11 +107,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             best = warp_min(lane < kWarps ? red[lane] : ~0ull);
             const bool has = best != ~0ull;
             const long li = has ? long(uint32_t(best)) - r0 : 0;
-            for (int dst = 0; dst < C; ++dst) {  // this CTA's candidate -> slot [par][rank] of every CTA
+            // this CTA's candidate -> slot [par][rank] of every CTA: lane w carries row word w
+            uint64_t rw = 0;
+            if (has && lane < words)
+                rw = rows_in_smem ? s_rows[long(lane) * per + li] : g_inc[(r0 + li) * long(words) + lane];
+            for (int dst = 0; dst < C; ++dst) {
                 Xch* x = cl.map_shared_rank(&xch[par * kMaxCluster + rank], dst);
                 if (lane == 0) x->key = best;
                 if (has)
-                    for (int w = lane; w < words; w += 32) x->row[w] = rows[li * words + w];
+                    for (int w = lane; w < words; w += 32)
+                        x->row[w] = w == lane ? rw : (rows_in_smem ? s_rows[long(w) * per + li] : g_inc[(r0 + li) * long(words) + w]);
             }
         }
         cl.sync();
@@ -109,6 +132,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (rank == 0 && tid == 0) order[step] = int32_t(uint32_t(win));
     }
 }
+
+thread_local RerankStats g_stats;
 
 // per-thread device scratch, grown on demand and kept (no allocator traffic per batch)
 struct Scratch {
@@ -152,11 +177,15 @@ std::vector<size_t> rerank_chain_device(const uint64_t* rows, size_t m, size_t w
         TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&sc.order), sc.cap_order * 4));
     }
     TKV_CUDA_CHECK(cudaMemcpyAsync(sc.inc, rows, m * words * 8, cudaMemcpyHostToDevice, s));
-    ensure_smem_optin(reinterpret_cast<const void*>(rerank_cluster_kernel), int(smem));
-    static thread_local int nonportable_dev = -1;
-    if (nonportable_dev != dev) {
-        TKV_CUDA_CHECK(cudaFuncSetAttribute(rerank_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        nonportable_dev = dev;
+    using KernelFn = void (*)(const uint64_t*, int, int, int, int, int, int32_t*);
+    const KernelFn kern = words <= 4 ? rerank_cluster_kernel<4> : words <= 8 ? rerank_cluster_kernel<8>
+                          : words <= 16 ? rerank_cluster_kernel<16> : rerank_cluster_kernel<kMaxWords>;
+    ensure_smem_optin(reinterpret_cast<const void*>(kern), int(smem));
+    static thread_local std::vector<const void*> nonportable;  // (kernel, device) pairs opted in
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kern) ^ uintptr_t(dev));
+    if (std::find(nonportable.begin(), nonportable.end(), key) == nonportable.end()) {
+        TKV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        nonportable.push_back(key);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(C));
@@ -170,20 +199,42 @@ std::vector<size_t> rerank_chain_device(const uint64_t* rows, size_t m, size_t w
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TKV_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rerank_cluster_kernel, static_cast<const uint64_t*>(sc.inc), int(m), int(words),
-                                      int(first), int(per), int(in_smem), sc.order));
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    static thread_local int ev_dev = -1;
+    if (ev_dev != dev) {
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[0]));
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[1]));
+        ev_dev = dev;
+    }
+    TKV_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    TKV_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<const uint64_t*>(sc.inc), int(m), int(words), int(first),
+                                      int(per), int(in_smem), sc.order));
+    TKV_CUDA_CHECK(cudaEventRecord(ev[1], s));
     std::vector<int32_t> ord(m);
     TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), sc.order, m * 4, cudaMemcpyDeviceToHost, s));
     TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0;
+    TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    g_stats.kernel_ms = ms;
+    g_stats.n_classes = double(m);
+    g_stats.cluster = C;
     return std::vector<size_t>(ord.begin(), ord.end());
 }
 
 std::vector<size_t> rerank_device(const uint64_t* inc, size_t n, size_t words, uint64_t seed, tablekv::AnchorMode mode,
                                   cudaStream_t s) {
     if (words > size_t(kMaxWords)) throw std::invalid_argument("device rerank supports up to 4096 tables");
+    const auto t0 = std::chrono::steady_clock::now();
+    g_stats = RerankStats{};
     const tablekv::RerankClasses rc = tablekv::rerank_classes(inc, n, words, seed, mode);
+    g_stats.classes_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (rc.n_classes() == 0) return rc.empty;
-    return tablekv::expand_class_chain(rc, rerank_chain_device(rc.rows.data(), rc.n_classes(), words, rc.anchor_class, s));
+    auto out = tablekv::expand_class_chain(rc, rerank_chain_device(rc.rows.data(), rc.n_classes(), words, rc.anchor_class, s));
+    g_stats.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
+RerankStats last_rerank_stats() { return g_stats;
 }
 
 }  // namespace tkv

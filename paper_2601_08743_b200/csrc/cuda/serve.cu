@@ -595,6 +595,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             if (d_segs_s) {
                 fa.gather_pool = pool_.base();
                 fa.gather_page_bytes = P;
+                fa.gather_pool_bytes = P * size_t(pool_.n_pages());
                 fa.gather_pages = d_pages_s;
                 fa.gather_segs = d_segs_s;
                 fa.gather_n_segs = int(segs.size());
@@ -602,12 +603,12 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 fa.gather_in = in_dt_s;
                 fa.gather_chunks = d_chunks_s;
                 fa.gather_n_chunks = n_chunks_s;
-                static const bool paged_v = [] {  // TKV_PAGED_V=0 keeps V in the gathered slab (A/B)
+                static const bool paged_v = [] {  // TKV_PAGED_V=0 / TKV_PAGED_K=0: gathered slab (A/B)
                     const char* e = std::getenv("TKV_PAGED_V");
                     return !(e && std::string(e) == "0");
                 }();
                 fa.paged_v = paged_v;
-                static const bool paged_k = [] {  // TKV_PAGED_K=0 gathers rotated K into a slab (A/B)
+                static const bool paged_k = [] {
                     const char* e = std::getenv("TKV_PAGED_K");
                     return !(e && std::string(e) == "0");
                 }();

@@ -87,6 +87,12 @@ BatchTrace plan_batch(const std::vector<std::vector<int>>& tables, const std::ve
 // rerank_packed (csrc/host/rerank.cpp) on the GPU: identical permutation, one CTA runs the chain
 std::vector<size_t> rerank_device(const uint64_t* inc, size_t n, size_t words, uint64_t seed, tablekv::AnchorMode mode,
                                   cudaStream_t s);
+// the calling thread's last rerank_device: host class reduction, chain kernel (CUDA events), whole call
+struct RerankStats {
+    double classes_ms = 0, kernel_ms = 0, total_ms = 0, n_classes = 0;
+    int cluster = 0;
+};
+RerankStats last_rerank_stats();
 constexpr size_t kDeviceRerankMin = 512;  // batches at least this large rerank on the GPU
 // table -> [first, last] windows during which the executor keeps it published for peers
 std::unordered_map<int, std::vector<std::pair<int, int>>> residency_intervals(const BatchTrace& bt);

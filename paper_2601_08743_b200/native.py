@@ -74,6 +74,7 @@ _sig("tkv_trie_query", _vp, _i32p, C.c_size_t, C.c_size_t, C.POINTER(C.c_int), C
 _sig("tkv_trie_match_all", _vp, _i32p, C.c_size_t, _i64p, C.c_size_t, C.POINTER(C.c_size_t), _u64p)
 _sig("tkv_rerank", _u64p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int, C.c_int, _u64p)
 _sig("tkv_rerank_device", C.c_int, _u64p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int, _u64p)
+_sig("tkv_rerank_device_stats", C.POINTER(C.c_double), C.c_int)
 _sig("tkv_cache_create", C.c_size_t, C.c_int, _i32p, C.c_size_t, C.POINTER(_vp))
 _sig("tkv_cache_destroy", _vp, res=None)
 _sig("tkv_cache_get", _vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int))
@@ -215,11 +216,13 @@ class Trie:
 def pack_incidence(table_sets, n_bits):
     words = max(1, (n_bits + 63) // 64)
     inc = np.zeros((len(table_sets), words), np.uint64)
-    for i, ts in enumerate(table_sets):
-        for t in ts:
-            if t < 0 or t >= n_bits:
-                raise ValueError("table id out of range")
-            inc[i, t >> 6] |= np.uint64(1) << np.uint64(t & 63)
+    lens = np.fromiter((len(ts) for ts in table_sets), np.int64, len(table_sets))
+    if lens.sum():
+        ids = np.fromiter((t for ts in table_sets for t in ts), np.int64, int(lens.sum()))
+        if ids.min() < 0 or ids.max() >= n_bits:
+            raise ValueError("table id out of range")
+        rows = np.repeat(np.arange(len(table_sets)), lens)
+        np.bitwise_or.at(inc, (rows, ids >> 6), np.left_shift(np.uint64(1), (ids & 63).astype(np.uint64)))
     return inc
 
 
@@ -239,6 +242,14 @@ def rerank_device(table_sets, n_bits, seed=1, mode="seeded", device=0):
     _check(_lib.tkv_rerank_device(device, _ptr(inc, C.c_uint64), inc.shape[0], inc.shape[1], seed,
                                   int(mode == "fixed_first"), _ptr(perm, C.c_uint64)))
     return [int(x) for x in perm]
+
+
+def rerank_device_stats():
+    """The calling thread's last rerank_device: host class reduction ms, chain kernel ms (CUDA events),
+    whole call ms, distinct table sets, cluster CTAs."""
+    v = (C.c_double * 5)()
+    _check(_lib.tkv_rerank_device_stats(v, 5))
+    return dict(zip(("classes_ms", "kernel_ms", "call_ms", "classes", "cluster"), list(v)))
 
 
 POLICIES = {"lru": 0, "fifo": 1, "lfu": 2}

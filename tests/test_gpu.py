@@ -530,23 +530,41 @@ def _paged_logits(tmp_path, tag, env_over):
     return np.load(out)
 
 
-@pytest.mark.parametrize("variant", [{"TKV_PAGED_V": "0"}, {"TKV_K_HEAD_MAJOR": "0"}])
-def test_paged_v_and_head_major_k_bit_identical_to_slab(tmp_path, variant):
-    """With the rotated-K gather (TKV_PAGED_K=0): paged V (the attention reads V straight from the
-    pool pages) and the head-major K slab move the same bytes to the same smem tiles as the
-    gathered row-major slab: the served logits must be bit-identical, not merely within tolerance."""
-    base = _paged_logits(tmp_path, "base", {"TKV_PAGED_K": "0"})
-    other = _paged_logits(tmp_path, "var", dict(variant, TKV_PAGED_K="0"))
+def test_tma_and_lsu_slab_gathers_bit_identical(tmp_path):
+    """Slab mode (TKV_PAGED_K=0: the gather writes rotated K and V into the one-layer slab, the
+    attention reads it by TMA): the TMA-staged gather and the 16-byte LSU gather (TKV_GATHER=lsu)
+    compute the same rotation on the same rows, so the served logits are bit-identical."""
+    base = _paged_logits(tmp_path, "tma", {"TKV_PAGED_K": "0"})
+    other = _paged_logits(tmp_path, "lsu", {"TKV_PAGED_K": "0", "TKV_GATHER": "lsu"})
     assert base.shape == other.shape and np.isfinite(base).all()
     assert np.array_equal(base.view(np.uint32), other.view(np.uint32))
 
 
-def test_paged_k_rotated_in_smem_matches_gathered_slab(tmp_path):
-    """Paged K (default: raw K rows copied from the pages into the attention's smem ring and rotated
-    there, cos/sin advanced by a per-thread angle recurrence from the f32 table) against the
-    gathered, table-rotated K slab: a rotated element can differ by one bf16 ulp where the
-    recurrence's ~1e-6 relative drift crosses a rounding boundary, so logits agree to 1e-2 (not
-    bit-exact) and the first token is the same wherever the slab's top-2 margin exceeds 2e-2."""
+def test_folded_rmsnorm_matches_separate_norm_kernels(tmp_path):
+    """RMSNorm folded into the GEMMs (default: the residual GEMMs write bf16(x) and per-128-column
+    sums of squares, the next projection scales its accumulator rows) against the separate norm
+    kernels (TKV_NORM_FOLD=0): the projection input is rounded before instead of after the scaling,
+    so logits agree to 2e-2 with the same first token wherever the top-2 margin exceeds 4e-2; and
+    the fold is deterministic (no atomics): two runs are bit-identical."""
+    fold = _paged_logits(tmp_path, "fold", {})
+    fold2 = _paged_logits(tmp_path, "fold2", {})
+    sep = _paged_logits(tmp_path, "sep", {"TKV_NORM_FOLD": "0"})
+    assert np.array_equal(fold.view(np.uint32), fold2.view(np.uint32))
+    assert np.isfinite(fold).all() and np.abs(fold - sep).max() <= 2e-2
+    top2 = np.sort(sep, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 4e-2
+    assert clear.sum() >= len(clear) // 2
+    assert np.array_equal(fold.argmax(1)[clear], sep.argmax(1)[clear])
+
+
+def test_paged_prefix_matches_gathered_slab(tmp_path):
+    """Paged prefix (default: K and V rows TMA'd from the pool pages into the attention's smem rings
+    — 8-row boxes for runs inside one segment and page, single rows across boundaries (64 KiB pages
+    here, so many) — and K rotated there, cos/sin advanced by a per-thread angle recurrence from the
+    f32 table) against the gathered, table-rotated slab: a rotated element can differ by one bf16
+    ulp where the recurrence's ~1e-6 relative drift crosses a rounding boundary, so logits agree to
+    1e-2 (not bit-exact) and the first token is the same wherever the slab's top-2 margin exceeds
+    2e-2."""
     paged = _paged_logits(tmp_path, "paged", {})[:, :330]
     slab = _paged_logits(tmp_path, "slab", {"TKV_PAGED_K": "0"})[:, :330]
     assert paged.shape == slab.shape and np.isfinite(paged).all()
