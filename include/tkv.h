@@ -73,7 +73,7 @@ int tkv_rerank(const uint64_t* inc, size_t n, size_t words, uint64_t seed, int f
 int tkv_rerank_device(int device, const uint64_t* inc, size_t n, size_t words, uint64_t seed, int fixed_first,
                       uint64_t* perm);
 /* the calling thread's last tkv_rerank_device: out = {host class reduction ms, chain kernel ms (CUDA
- * events), whole call ms, distinct table sets, cluster CTAs} */
+ * events), whole call ms, distinct table sets, cluster CTAs (0: the compact single-CTA chain)} */
 int tkv_rerank_device_stats(double* out, int n);
 
 /* ---- fast-tier policy bookkeeping (tiered_cache.hpp:69-113) over a metadata slow tier --- */

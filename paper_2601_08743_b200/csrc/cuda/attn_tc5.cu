@@ -674,9 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(b_sfull(st), int(gi & 1));
                 if (warp == 4 && lane == 0) TR(5, gi);
                 fence_after();
-                // S is read from TMEM twice, 32 columns at a time with the next chunk's load in flight:
-                // pass 1 takes the row max, pass 2 the exponentials. Two 32-register chunks instead of
-                // the whole 128-column row keep the softmax warps far from their register cap.
+                // S row -> registers, row max, conditional rescale, then exponentials -> P over S's first
+                // 64 columns (TKV_ATTN_TWOPASS: the round-1 variant reading S twice in 32-column chunks)
                 const bool masked = !(ctx && base_j + BN <= sq.n_ctx);  // full prefix tiles skip the mask
                 const int lim = masked ? min(seg_end, causal + 1) - base_j : BN;  // columns [lo_c, lim) visible
                 const int lo_c = masked ? lo - base_j : 0;
@@ -687,7 +686,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (c0 + i >= lim || c0 + i < lo_c) v[i] = 0xff800000u;  // -inf
                     }
                 };
+#ifdef TKV_ATTN_TWOPASS
                 uint32_t ua[32], ub[32];
+#endif
                 // row max as four independent 3-input max chains (FMNMX3)
                 float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
                 auto max_chunk = [&](const uint32_t* v) {
@@ -697,6 +698,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int q = 0; q < 4; ++q)
                             m4[q] = fmaxf(fmaxf(m4[q], __uint_as_float(v[i + 2 * q])), __uint_as_float(v[i + 2 * q + 1]));
                 };
+#ifndef TKV_ATTN_TWOPASS
+                // one pass: the whole 128-column S row into registers (4 loads, one wait) — TMEM reads
+                // run at 64 B/clk per SM, so S is read once per tile, not twice
+                uint32_t sv[128];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tmem_ld32_async(tS + 32 * k, sv + 32 * k);
+                tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) reg_fence32(sv + 32 * k);
+                if (warp == 4 && lane == 0) TR(12, gi);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mask_chunk(sv + 32 * k, 32 * k);
+                    max_chunk(sv + 32 * k);
+                }
+#else
                 tmem_ld32_async(tS, ua);
                 tmem_wait_ld();
                 reg_fence32(ua);
@@ -713,25 +730,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         reg_fence32(nxt);
                     }
                 }
+#endif
                 float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 mx *= sl2;  // scale > 0: the max commutes with it
                 // conditional rescale: keep the running max unless it grows by more than 8 (x256)
+                // (O is rescaled after P is written, before P is published: the S registers are dead
+                // by then, and PV(t) cannot start before the P-ready arrival)
                 const bool grow = mx > m_run + 8.f;
-                if (t > 0 && __any_sync(0xffffffffu, grow)) {
-                    mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
-                    fence_after();
-                    const float corr = grow ? ex2(m_run - mx) : 1.f;
-#pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        float o[32];
-                        tmem_ld32(tO + c, o);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] *= corr;
-                        tmem_st32(tO + c, o);
-                    }
-                    if (grow) l_run *= corr;
-                }
-                if (grow) m_run = mx;
+                const bool any_grow = t > 0 && __any_sync(0xffffffffu, grow);
+                const float corr = grow ? ex2(m_run - mx) : 1.f;
+                if (grow) l_run *= corr, m_run = mx;
                 if (warp == 4 && lane == 0) TR(13, gi);
                 // rows past the item's tokens get P = 0 through the bias (-inf)
                 const float nb = !live ? -INFINITY : (m_run == -INFINITY ? 0.f : -m_run);
@@ -740,15 +748,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // lands on columns [16k, 16k+16), all of which pass 2 has already read)
                 const uint64_t sl2x2 = pack_f32x2(sl2, sl2), nbx2 = pack_f32x2(nb, nb);
                 uint64_t acc[2] = {0ull, 0ull};
+#ifdef TKV_ATTN_TWOPASS
                 tmem_ld32_async(tS, ua);
                 tmem_wait_ld();
                 reg_fence32(ua);
+#endif
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
+#ifndef TKV_ATTN_TWOPASS
+                    uint32_t* cur = sv + 32 * k;  // already masked
+#else
                     uint32_t* cur = (k & 1) ? ub : ua;
                     uint32_t* nxt = (k & 1) ? ua : ub;
                     if (k < 3) tmem_ld32_async(tS + 32 * (k + 1), nxt);
                     mask_chunk(cur, 32 * k);
+#endif
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
@@ -777,16 +791,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     }
                     tmem_st16(tS + 16 * k, pk);
+#ifdef TKV_ATTN_TWOPASS
                     if (k < 3) {
                         tmem_wait_ld();
                         reg_fence32(nxt);
                     }
+#endif
                 }
                 float s0, s1, s2, s3;
                 unpack_f32x2(acc[0], s0, s1);
                 unpack_f32x2(acc[1], s2, s3);
                 l_run += (s0 + s1) + (s2 + s3);
                 if (warp == 4 && lane == 0) TR(14, gi);
+                if (any_grow) {
+                    mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
+                    fence_after();
+#pragma unroll
+                    for (int c = 0; c < D; c += 32) {
+                        float o[32];
+                        tmem_ld32(tO + c, o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] *= corr;
+                        tmem_st32(tO + c, o);
+                    }
+                }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
                 __syncwarp();

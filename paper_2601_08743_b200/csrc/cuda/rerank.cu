@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstring>
 #include <chrono>
 #include <vector>
 
@@ -26,7 +27,7 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxWords = 64;    // tables up to 4096
 constexpr int kMaxCluster = 16;  // non-portable cluster size (opted in below)
@@ -133,6 +134,120 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// Compact chain on ONE CTA (no cluster barrier per step): when every distinct table set fits a
+// 128-bit window of two consecutive incidence words (a query's tables come from one database), a
+// row is (w0, bits of words w0 and w0 + 1, popcount) — 19 bytes — so 10k classes fit one SM's
+// shared memory. distance(cur, row) = |cur| + |row| - 2 |cur & row|, the intersection read off the
+// overlap of the two windows: the same integer as the XOR popcount, the same (distance, slot) key.
+constexpr int kCompactThreads = 1024;
+constexpr size_t kCompactRowBytes = 16 + 2 + 1;
+
+__global__ void __launch_bounds__(kCompactThreads, 1)
+    rerank_compact_kernel(const ulonglong2* __restrict__ g_bits, const uint16_t* __restrict__ g_w0,
+                          const uint8_t* __restrict__ g_pc, int n, int first, int32_t* __restrict__ order) {
+    extern __shared__ __align__(16) uint8_t csm[];
+    ulonglong2* s_bits = reinterpret_cast<ulonglong2*>(csm);
+    uint16_t* s_w0 = reinterpret_cast<uint16_t*>(s_bits + n);
+    uint8_t* s_pc = reinterpret_cast<uint8_t*>(s_w0 + n);
+    __shared__ unsigned long long red[32];
+    __shared__ unsigned long long win_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n; i += kCompactThreads) s_bits[i] = g_bits[i], s_w0[i] = g_w0[i], s_pc[i] = g_pc[i];
+    uint32_t used = 0;
+    if (first % kCompactThreads == tid) used |= 1u << (first / kCompactThreads);
+    if (tid == 0) order[0] = first;
+    __syncthreads();
+    int cw = s_w0[first], cpc = s_pc[first];
+    ulonglong2 cb = s_bits[first];
+    for (int step = 1; step < n; ++step) {
+        unsigned long long best = ~0ull;
+        int j = 0;
+        for (int i = tid; i < n; i += kCompactThreads, ++j) {
+            if ((used >> j) & 1u) continue;
+            const ulonglong2 b = s_bits[i];
+            const int w = s_w0[i];
+            const uint64_t x0 = w == cw ? cb.x : (w == cw + 1 ? cb.y : 0ull);  // cur's words w, w + 1
+            const uint64_t x1 = w + 1 == cw ? cb.x : (w == cw ? cb.y : 0ull);
+            const uint32_t d = uint32_t(cpc + s_pc[i] - 2 * (__popcll(x0 & b.x) + __popcll(x1 & b.y)));
+            const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | uint32_t(i);
+            best = key < best ? key : best;
+        }
+        best = warp_min(best);
+        if (lane == 0) red[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            best = warp_min(red[lane]);
+            if (lane == 0) win_s = best;
+        }
+        __syncthreads();
+        const int wi = int(uint32_t(win_s));
+        cw = s_w0[wi], cpc = s_pc[wi], cb = s_bits[wi];
+        if (wi % kCompactThreads == tid) used |= 1u << (wi / kCompactThreads);
+        if (tid == 0) order[step] = wi;
+    }
+}
+
+// Window chain on ONE CTA with the rows in REGISTERS: when every distinct table set lies within 64
+// consecutive table ids (one database's tables), a row is (first id b0, 64 bits from b0, popcount)
+// and thread t keeps rows t + 1024 j for j < R in registers, so the per-step scan reads no shared
+// memory at all; the intersection with the current row is a funnel of the two windows. Keys are
+// 32-bit: (distance << 14) | slot, so the argmin is the same (distance, lowest slot) order.
+constexpr int kWinThreads = 1024;
+
+template <int R>
+__global__ void __launch_bounds__(kWinThreads, 1)
+    rerank_window_kernel(const uint64_t* __restrict__ g_bits, const uint16_t* __restrict__ g_b0,
+                         const uint8_t* __restrict__ g_pc, int n, int first, int32_t* __restrict__ order) {
+    extern __shared__ __align__(16) uint8_t wsm[];
+    uint64_t* s_bits = reinterpret_cast<uint64_t*>(wsm);
+    uint16_t* s_b0 = reinterpret_cast<uint16_t*>(s_bits + n);
+    uint8_t* s_pc = reinterpret_cast<uint8_t*>(s_b0 + n);
+    __shared__ uint32_t red[32];
+    __shared__ uint32_t win_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n; i += kWinThreads) s_bits[i] = g_bits[i], s_b0[i] = g_b0[i], s_pc[i] = g_pc[i];
+    uint64_t rb[R];
+    int rs[R];  // b0 | popcount << 16
+    uint32_t used = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int i = tid + j * kWinThreads;
+        rb[j] = i < n ? g_bits[i] : 0ull;
+        rs[j] = i < n ? int(g_b0[i]) | (int(g_pc[i]) << 16) : 0;
+        if (i >= n || i == first) used |= 1u << j;
+    }
+    if (tid == 0) order[0] = first;
+    __syncthreads();
+    uint64_t cb = s_bits[first];
+    int cb0 = s_b0[first], cpc = s_pc[first];
+    for (int step = 1; step < n; ++step) {
+        uint32_t best = ~0u;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int sh = (rs[j] & 0xffff) - cb0;
+            const uint64_t x = sh >= 64 || sh <= -64 ? 0ull : (sh >= 0 ? cb >> sh : cb << -sh);  // cur's bits at the row's window
+            const uint32_t d = uint32_t(cpc + (rs[j] >> 16) - 2 * __popcll(x & rb[j]));
+            const uint32_t key = (used >> j) & 1u ? ~0u : (d << 14) | uint32_t(tid + j * kWinThreads);
+            best = min(best, key);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) red[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            best = red[lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (lane == 0) win_s = best;
+        }
+        __syncthreads();
+        const int wi = int(win_s & 0x3fffu);
+        cb = s_bits[wi], cb0 = s_b0[wi], cpc = s_pc[wi];
+        if (wi % kWinThreads == tid) used |= 1u << (wi / kWinThreads);
+        if (tid == 0) order[step] = wi;
+    }
+}
+
 thread_local RerankStats g_stats;
 
 // per-thread device scratch, grown on demand and kept (no allocator traffic per batch)
@@ -143,10 +258,156 @@ struct Scratch {
     size_t cap_inc = 0, cap_order = 0;
 };
 
+std::vector<size_t> rerank_window_device(const std::vector<uint64_t>& bits, const std::vector<uint16_t>& b0,
+                                         const std::vector<uint8_t>& pc, size_t first, cudaStream_t s) {
+    const size_t m = bits.size();
+    static thread_local int dev_cached = -1;
+    static thread_local uint8_t* buf = nullptr;
+    static thread_local int32_t* ord_d = nullptr;
+    static thread_local size_t cap = 0;
+    int dev = 0;
+    TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    const size_t bytes = m * 8 + m * 2 + m;
+    if (dev_cached != dev || cap < m) {  // (a previous device's buffers are left to it)
+        if (dev_cached == dev) cudaFree(buf), cudaFree(ord_d);
+        cap = std::max<size_t>(m, 4096);
+        TKV_CUDA_CHECK(cudaMalloc(&buf, cap * 11 + 64));
+        TKV_CUDA_CHECK(cudaMalloc(&ord_d, cap * 4));
+        dev_cached = dev;
+    }
+    std::vector<uint8_t> host(bytes);
+    std::memcpy(host.data(), bits.data(), m * 8);
+    std::memcpy(host.data() + m * 8, b0.data(), m * 2);
+    std::memcpy(host.data() + m * 10, pc.data(), m);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(buf, host.data(), bytes, cudaMemcpyHostToDevice, s));
+    const size_t smem = bytes + 16;
+    using KernelFn = void (*)(const uint64_t*, const uint16_t*, const uint8_t*, int, int, int32_t*);
+    const KernelFn kern = m <= 4 * size_t(kWinThreads) ? rerank_window_kernel<4>
+                          : m <= 8 * size_t(kWinThreads) ? rerank_window_kernel<8>
+                          : m <= 12 * size_t(kWinThreads) ? rerank_window_kernel<12> : rerank_window_kernel<16>;
+    ensure_smem_optin(reinterpret_cast<const void*>(kern), int(smem));
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    static thread_local int ev_dev = -1;
+    if (ev_dev != dev) {
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[0]));
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[1]));
+        ev_dev = dev;
+    }
+    TKV_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    kern<<<1, kWinThreads, smem, s>>>(reinterpret_cast<const uint64_t*>(buf), reinterpret_cast<const uint16_t*>(buf + m * 8),
+                                      buf + m * 10, int(m), int(first), ord_d);
+    TKV_CUDA_CHECK(cudaGetLastError());
+    TKV_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    std::vector<int32_t> ord(m);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), ord_d, m * 4, cudaMemcpyDeviceToHost, s));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0;
+    TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    g_stats.kernel_ms = ms;
+    g_stats.n_classes = double(m);
+    g_stats.cluster = -1;  // register-window single-CTA chain
+    return std::vector<size_t>(ord.begin(), ord.end());
+}
+
+std::vector<size_t> rerank_compact_device(const std::vector<ulonglong2>& bits, const std::vector<uint16_t>& w0,
+                                          const std::vector<uint8_t>& pc, size_t first, cudaStream_t s) {
+    const size_t m = bits.size();
+    static thread_local int dev_cached = -1;
+    static thread_local uint8_t* buf = nullptr;
+    static thread_local int32_t* ord_d = nullptr;
+    static thread_local size_t cap = 0;
+    int dev = 0;
+    TKV_CUDA_CHECK(cudaGetDevice(&dev));
+    const size_t bytes = m * 16 + m * 2 + m + 64;
+    if (dev_cached != dev || cap < m) {  // (a previous device's buffers are left to it)
+        if (dev_cached == dev) cudaFree(buf), cudaFree(ord_d);
+        cap = std::max<size_t>(m, 4096);
+        TKV_CUDA_CHECK(cudaMalloc(&buf, cap * 19 + 64));
+        TKV_CUDA_CHECK(cudaMalloc(&ord_d, cap * 4));
+        dev_cached = dev;
+    }
+    std::vector<uint8_t> host(bytes);
+    std::memcpy(host.data(), bits.data(), m * 16);
+    std::memcpy(host.data() + m * 16, w0.data(), m * 2);
+    std::memcpy(host.data() + m * 18, pc.data(), m);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(buf, host.data(), bytes, cudaMemcpyHostToDevice, s));
+    const size_t smem = m * kCompactRowBytes + 16;
+    ensure_smem_optin(reinterpret_cast<const void*>(rerank_compact_kernel), int(smem));
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    static thread_local int ev_dev = -1;
+    if (ev_dev != dev) {
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[0]));
+        TKV_CUDA_CHECK(cudaEventCreate(&ev[1]));
+        ev_dev = dev;
+    }
+    TKV_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    rerank_compact_kernel<<<1, kCompactThreads, smem, s>>>(reinterpret_cast<const ulonglong2*>(buf),
+                                                            reinterpret_cast<const uint16_t*>(buf + m * 16), buf + m * 18,
+                                                            int(m), int(first), ord_d);
+    TKV_CUDA_CHECK(cudaGetLastError());
+    TKV_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    std::vector<int32_t> ord(m);
+    TKV_CUDA_CHECK(cudaMemcpyAsync(ord.data(), ord_d, m * 4, cudaMemcpyDeviceToHost, s));
+    TKV_CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0;
+    TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    g_stats.kernel_ms = ms;
+    g_stats.n_classes = double(m);
+    g_stats.cluster = 0;  // compact single-CTA chain
+    return std::vector<size_t>(ord.begin(), ord.end());
+}
+
 }  // namespace
 
 std::vector<size_t> rerank_chain_device(const uint64_t* rows, size_t m, size_t words, size_t first, cudaStream_t s) {
     if (m == 0) return {};
+    // register-window chain when every row's tables span < 64 consecutive ids (and < 16384 rows)
+    if (m <= 16 * size_t(kWinThreads) && m * 11 + 16 <= kSmemRowsCap) {
+        std::vector<uint64_t> bits(m);
+        std::vector<uint16_t> b0(m);
+        std::vector<uint8_t> pc(m);
+        bool ok = true;
+        for (size_t i = 0; i < m && ok; ++i) {
+            const uint64_t* r = rows + i * words;
+            long lo = -1, hi = -1;
+            int p = 0;
+            for (size_t w = 0; w < words; ++w)
+                if (r[w]) {
+                    if (lo < 0) lo = long(w) * 64 + __builtin_ctzll(r[w]);
+                    hi = long(w) * 64 + 63 - __builtin_clzll(r[w]);
+                    p += __builtin_popcountll(r[w]);
+                }
+            if (lo < 0) lo = hi = 0;
+            ok = hi - lo < 64 && lo < 65536;
+            if (!ok) break;
+            const size_t w = size_t(lo) >> 6, o = size_t(lo) & 63;
+            const uint64_t a = r[w], b = w + 1 < words ? r[w + 1] : 0ull;
+            bits[i] = o ? (a >> o) | (b << (64 - o)) : a;
+            b0[i] = uint16_t(lo);
+            pc[i] = uint8_t(p);
+        }
+        if (ok) return rerank_window_device(bits, b0, pc, first, s);
+    }
+    // compact single-CTA chain when every row lives in two consecutive words and the rows fit smem
+    if (m * kCompactRowBytes <= kSmemRowsCap && m <= size_t(kCompactThreads) * kMaxRowsPerThread) {
+        std::vector<ulonglong2> bits(m);
+        std::vector<uint16_t> w0(m);
+        std::vector<uint8_t> pc(m);
+        bool ok = true;
+        for (size_t i = 0; i < m && ok; ++i) {
+            const uint64_t* r = rows + i * words;
+            size_t lo = words, hi = 0;
+            int p = 0;
+            for (size_t w = 0; w < words; ++w)
+                if (r[w]) lo = std::min(lo, w), hi = w, p += __builtin_popcountll(r[w]);
+            if (lo == words) lo = hi = 0;
+            ok = hi <= lo + 1 && p < 256;
+            w0[i] = uint16_t(lo);
+            pc[i] = uint8_t(p);
+            bits[i] = make_ulonglong2(r[lo], lo + 1 < words ? r[lo + 1] : 0ull);
+        }
+        if (ok) return rerank_compact_device(bits, w0, pc, first, s);
+    }
     if (words > size_t(kMaxWords)) throw std::invalid_argument("device rerank supports up to 4096 tables");
     if (m > size_t(kMaxCluster) * kThreads * kMaxRowsPerThread) throw std::invalid_argument("device rerank: batch too large");
     // smallest cluster whose slices fit shared memory with at most 4 rows per thread; beyond 16

@@ -403,6 +403,27 @@ def test_device_rerank_distinct_sets_at_c5_scale(n, n_bits, per_db, seed):
     print("device rerank: %d queries x %d tables: %.1f ms" % (n, n_bits, ms))
 
 
+@pytest.mark.parametrize("n,n_bits,per_db,path", [(3000, 660, 60, -1), (9000, 660, 64, -1), (5000, 1024, 128, 0),
+                                                   (3000, 4096, 700, 1), (300, 130, 130, -1)])
+def test_device_rerank_each_chain_kernel(n, n_bits, per_db, path):
+    """Every device chain kernel against the host chain, each forced by the shape of the sets: the
+    register-window chain (every set inside 64 consecutive table ids, including windows that cross
+    a 64-bit word), the compact two-word chain (sets inside 128-table, word-aligned databases), and
+    the cluster chain (wider sets); rerank_device_stats reports which one ran (-1 / 0 / >= 1)."""
+    rng = np.random.default_rng(n)
+    sets = []
+    for i in range(n):
+        db = int(rng.integers(0, n_bits // per_db))
+        k = int(rng.integers(1, 12))
+        lo = db * per_db + (int(rng.integers(0, per_db - 63)) if path == -1 and per_db > 64 else 0)
+        span = min(64, per_db) if path == -1 else per_db
+        sets.append(sorted(set((lo + rng.integers(0, span, k)).tolist())))
+    dev = N.rerank_device(sets, n_bits, seed=3)
+    st = N.rerank_device_stats()
+    assert dev == N.rerank(sets, n_bits, seed=3)
+    assert (st["cluster"] >= 1) if path == 1 else st["cluster"] == path, st
+
+
 def test_load_dir_reference_and_bf16_images(tmp_path, f32_store):
     """Arena loader: the reference .kv directory and our bf16 .kvb precompute
     directory load straight into pinned memory; landed bytes equal the files' payloads."""
