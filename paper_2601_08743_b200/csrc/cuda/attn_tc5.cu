@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(b_pfull(st));
                 if (warp == 4 && lane == 0) TR(6, gi);
+                if (warp == 8 && lane == 0) TR(15, gi);  // stream 1's P ready
             }
             // ---- epilogue: O / l -> bf16 row, then O free for the next item
             const long gl = g + it.n_tiles - 1;

@@ -9,13 +9,13 @@ t = np.fromfile(sys.argv[1], np.uint32).reshape(16, 1024).astype(np.int64)
 t0 = t[10, 0]
 rel = lambda x: (x - t0) if x else -1
 names = ["K_issue", "V_issue", "mma_kfull", "QK_commit", "mma_pfull", "sm_sfull", "sm_pready", "", "", "K_ready", "",
-         "mma_vfull", "sm_sload", "sm_max", "sm_exp", "V_issued"]
+         "mma_vfull", "sm_sload", "sm_max", "sm_exp", "sm1_pready"]
 print("items: Q issue / epilogue done")
 for j in range(1024):
     if not t[8, j]:
         break
     print("  j=%d  %8d %8d" % (j, rel(t[8, j]), rel(t[7, j])))
-cols = [0, 9, 1, 15, 2, 3, 5, 12, 13, 14, 6, 4, 11]
+cols = [0, 9, 1, 11, 2, 5, 12, 13, 14, 6, 4, 15, 3]
 print("g     " + " ".join("%10s" % names[c] for c in cols))
 for g in range(1024):
     if not t[0, g]:
