@@ -366,6 +366,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         aa.k_own = static_cast<const __nv_bfloat16*>(k);
         aa.v_own = static_cast<const __nv_bfloat16*>(v_l);
         const bool streamed = a.gather_segs != nullptr;
+        if (a.layer_ready && a.layer_ready[l]) TKV_CUDA_CHECK(cudaStreamWaitEvent(s, a.layer_ready[l]));
         if (streamed && !paged) {
             cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing_) {

@@ -152,4 +152,19 @@ void copy_table_to_pages(const TableImage& img, PagePool& pool, const std::vecto
     }
 }
 
+void copy_image_range_to_pages(const TableImage& img, PagePool& pool, const std::vector<int32_t>& pages, size_t off,
+                               size_t bytes, cudaStream_t s) {
+    const size_t P = pool.page_bytes();
+    if (off + bytes > img.bytes || pages.size() * P < img.bytes) throw std::logic_error("image range outside the table pages");
+    const size_t end = off + bytes;
+    while (off < end) {  // one DMA transfer per run of physically adjacent pages
+        size_t i = off / P;
+        size_t stop = std::min(end, (i + 1) * P);
+        while (stop < end && i + 1 < pages.size() && pages[i + 1] == pages[i] + 1) ++i, stop = std::min(end, (i + 1) * P);
+        TKV_CUDA_CHECK(cudaMemcpyAsync(pool.base() + size_t(pages[off / P]) * P + off % P, img.host + off, stop - off,
+                                       cudaMemcpyHostToDevice, s));
+        off = stop;
+    }
+}
+
 }  // namespace tkv

@@ -89,5 +89,8 @@ enum class CopyEngine : int { dma = 0, sm = 1 };
 // Enqueue the copy of a table image into `pages` on `s`.
 void copy_table_to_pages(const TableImage& img, PagePool& pool, const std::vector<int32_t>& pages, CopyEngine eng,
                          int sm_ctas, cudaStream_t s);
+// DMA copy of image bytes [off, off + bytes) into their place in `pages` (layer-ordered loads)
+void copy_image_range_to_pages(const TableImage& img, PagePool& pool, const std::vector<int32_t>& pages, size_t off,
+                               size_t bytes, cudaStream_t s);
 
 }  // namespace tkv

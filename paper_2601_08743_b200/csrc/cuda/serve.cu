@@ -415,6 +415,13 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         const char* e = std::getenv("TKV_HOST_LEAD");
         return e ? std::atoi(e) : 2;
     }();
+    static const bool layered_env = [] {  // TKV_LAYERED_LOADS=1: layer-ordered demand copies (measured slower)
+        const char* e = std::getenv("TKV_LAYERED_LOADS");
+        return e && std::atoi(e) != 0;
+    }();
+    constexpr int kLayerChunk = 4;
+    const int n_lchunks = (L + kLayerChunk - 1) / kLayerChunk;
+    std::vector<std::vector<cudaEvent_t>> lchunk_ev(plan.windows.size(), std::vector<cudaEvent_t>(size_t(n_lchunks), nullptr));
     hp_tick(hp_plan);
     for (size_t wi = 0; wi < plan.windows.size(); ++wi) {
         if (host_lead > 0 && wi >= size_t(host_lead) && win_end[wi - host_lead])
@@ -484,7 +491,28 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         cudaEvent_t d0 = evp.get(), p0 = evp.get(), d1 = evp.get(), p1 = evp.get();
         hp_tick(hp_rest);
         TKV_CUDA_CHECK(cudaEventRecord(d0, ds_));
-        flush_copies(ds_);
+        // Layer-ordered demand loads: the window's tables are copied kLayerChunk layers at a time
+        // (K rows then V rows of those layers, image byte ranges [l0 T, l1 T) rows), an event after
+        // each chunk; the prefill starts after the first chunk and each layer's attention waits
+        // only for its own chunk — the projections of early layers overlap the later layers' H2D.
+        // (Whole tables when a peer may read the published pages, for the SM copy kernel, and for
+        // the f32 models whose prefix is gathered for all layers at once.)
+        const bool layered = layered_env && stream_ctx && !peering && opts.engine == CopyEngine::dma;
+        if (layered) {
+            for (int c = 0; c < n_lchunks; ++c) {
+                const int l0 = c * kLayerChunk, l1 = std::min(L, l0 + kLayerChunk);
+                for (const auto& pc : pending) {
+                    if (pc.st != ds_) continue;
+                    const size_t blk = pc.img->bytes / size_t(2 * L);  // one layer of K (or V) rows
+                    copy_image_range_to_pages(*pc.img, pool_, pc.pages, size_t(l0) * blk, size_t(l1 - l0) * blk, ds_);
+                    copy_image_range_to_pages(*pc.img, pool_, pc.pages, size_t(L + l0) * blk, size_t(l1 - l0) * blk, ds_);
+                }
+                lchunk_ev[wi][size_t(c)] = evp.get();
+                TKV_CUDA_CHECK(cudaEventRecord(lchunk_ev[wi][size_t(c)], ds_));
+            }
+        } else {
+            flush_copies(ds_);
+        }
         TKV_CUDA_CHECK(cudaEventRecord(d1, ds_));
         TKV_CUDA_CHECK(cudaEventRecord(p0, ps_));
         flush_copies(ps_);
@@ -502,8 +530,11 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             TKV_CUDA_CHECK(cudaEventRecord(x1, xs_));
         }
 
-        // ---- compute(wi): needs this window's demand loads and every earlier prefetch
-        TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, d1));
+        // ---- compute(wi): needs this window's demand loads and every earlier prefetch (a window
+        // that opens its own compute group and was loaded layer by layer: only the first chunk here,
+        // the rest per layer inside the prefill)
+        const bool layer_waits = layered && group_first == wi && closes[wi];
+        TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, layer_waits ? lchunk_ev[wi][0] : d1));
         if (prev_pref) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, prev_pref));
         prev_pref = p1;
         if (x1) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, x1));
@@ -613,6 +644,13 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                     return !(e && std::string(e) == "0");
                 }();
                 fa.paged_k = paged_k;
+            }
+            std::vector<cudaEvent_t> layer_ready;
+            if (layered_env && stream_ctx && !peering && opts.engine == CopyEngine::dma && group_first == wi &&
+                !lchunk_ev[wi].empty() && lchunk_ev[wi][0]) {
+                layer_ready.resize(size_t(L));
+                for (int l = 0; l < L; ++l) layer_ready[size_t(l)] = lchunk_ev[wi][size_t(l / kLayerChunk)];
+                fa.layer_ready = layer_ready.data();
             }
             fa.logit_rows = static_cast<const int32_t*>(ring.upload(logit_rows.data(), logit_rows.size() * 4, cs_));
             fa.logit_rows_host = logit_rows.data();
