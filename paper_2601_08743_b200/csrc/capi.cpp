@@ -179,6 +179,7 @@ json serve_result_json(const tkv::ServeResult& R) {
             {"argmax", R.argmax},
             {"window_of", R.window_of},
             {"window_end_ms", R.window_end_ms},
+            {"window_timeline_ms", R.window_timeline},
             {"trace", tr},
             {"counters", {R.counters.hits, R.counters.misses, R.counters.swaps, R.counters.prefetch_loads}},
             {"h2d_bytes", R.h2d_bytes},

@@ -666,6 +666,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // blocks: a row sees own keys [first key of its group block, itself]
             const int lo = a.mode == 1 ? a.row_lo[sq.q_row0 + tok] : 0;
             float m_run = -INFINITY, l_run = 0.f;
+            // a warp whose 32 rows are all past the item's tokens (short suffixes) skips the TMEM
+            // reads, exponentials and P writes: its O rows are never stored, so its P may stay
+            // whatever S left there; it still paces on S-ready / PV-done so its arrivals stay in phase
+            const bool wdead = __all_sync(0xffffffffu, !live);
             for (int t = 0; t < it.n_tiles; ++t) {
                 const long gi = g + t;
                 const bool ctx = t < it.n_ctx_tiles;
@@ -673,6 +677,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int seg_end = ctx ? sq.n_ctx : sq.n_ctx + sq.n_own;
                 mbar_wait(b_sfull(st), int(gi & 1));
                 if (warp == 4 && lane == 0) TR(5, gi);
+                if (wdead) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(b_pfull(st));
+                    continue;
+                }
                 fence_after();
                 // S row -> registers, row max, conditional rescale, then exponentials -> P over S's first
                 // 64 columns (TKV_ATTN_TWOPASS: the round-1 variant reading S twice in 32-column chunks)
@@ -829,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16* dst = a.out + long(sq.q_row0 + tok) * qw + (it.kvh * G + r % G) * D;
 #pragma unroll
-            for (int c = 0; c < D; c += 32) {
+            for (int c = 0; c < (wdead ? 0 : D); c += 32) {
                 float o[32];
                 tmem_ld32(tO + c, o);
                 if (live) {

@@ -371,6 +371,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     }
     std::vector<cudaEvent_t> win_end(plan.windows.size());
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dspan, pspan;
+    std::vector<cudaEvent_t> cstart(plan.windows.size(), nullptr);
     cudaEvent_t prev_pref = nullptr;
     R.window_of.assign(plan.queries.size(), 0);
     R.argmax.assign(plan.queries.size(), -1);
@@ -538,6 +539,8 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         if (prev_pref) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, prev_pref));
         prev_pref = p1;
         if (x1) TKV_CUDA_CHECK(cudaStreamWaitEvent(cs_, x1));
+        cstart[wi] = evp.get();  // compute(wi) may start here (its waits are satisfied)
+        TKV_CUDA_CHECK(cudaEventRecord(cstart[wi], cs_));
         // publish what landed for this window (still resident with the same pages)
         for (auto& [t, pages] : pub_now) {
             auto it = resident.find(t);
@@ -726,6 +729,9 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
         const double d = elapsed(dspan[i].first, dspan[i].second);
         R.copy_demand_ms += d;
         R.copy_busy_ms += d + elapsed(pspan[i].first, pspan[i].second);
+        // per window: demand copies [start, end), compute(w) ready, window end (ms from submission)
+        R.window_timeline.push_back({elapsed(t0, dspan[i].first), elapsed(t0, dspan[i].second),
+                                     cstart[i] ? elapsed(t0, cstart[i]) : -1.0, R.window_end_ms[i]});
     }
     if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms, R.gather_bytes);
     if (opts.keep_logits) R.logits = std::move(logits_host);

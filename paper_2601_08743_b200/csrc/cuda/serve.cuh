@@ -4,6 +4,8 @@
 // stream, events for TTFT. proj/src/pipeline.cpp:310-342 (run_batch) is the reference caller.
 #pragma once
 
+#include <array>
+
 #include <cuda_runtime.h>
 
 #include <string>
@@ -57,6 +59,7 @@ struct ServeResult {
     std::vector<float> logits;             // [served][vocab_padded] when keep_logits
     std::vector<int> window_of;            // per served query
     std::vector<double> window_end_ms;
+    std::vector<std::array<double, 4>> window_timeline;  // demand copy start / end, compute ready, end
     std::vector<TraceEvent> trace;
     tablekv::CacheCounters counters;
     size_t h2d_bytes = 0, meta_bytes = 0;
