@@ -33,6 +33,7 @@ struct AttnArgs {
     // rotated in shared memory at its prefix positions with the f32 RoPE tables [pos][head_dim/2];
     // vpool = pool base, page_ids / segs / layer / layers locate the rows, no slab
     bool kpaged = false;
+    const int32_t* seq_seg0 = nullptr;   // paged mode: first segment of each sequence (no search)
     int rows_shift = 0;
     const float* cos_f = nullptr;
     const float* sin_f = nullptr;

@@ -246,6 +246,13 @@ struct SegCursor {
         sg = a.segs[lo];
         next_row0 = lo + 1 < a.n_segs ? a.segs[lo + 1].out_row0 : 0x7fffffff;
     }
+    // start at a known segment (the sequence's first) and walk forward to the one holding vr
+    __device__ __forceinline__ void start(const AttnArgs& a, int s0, int vr) {
+        seg = s0;
+        sg = a.segs[s0];
+        next_row0 = s0 + 1 < a.n_segs ? a.segs[s0 + 1].out_row0 : 0x7fffffff;
+        advance(a, vr);
+    }
     __device__ __forceinline__ void advance(const AttnArgs& a, int vr) {
         while (vr >= next_row0) {
             ++seg;
@@ -440,7 +447,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         long g = 0;
         for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
             const Item it = item(w);
-            if (it.n_ctx_tiles && lane < 16) cur.seek(a, it.sq.ctx_row0 + min(8 * lane, it.sq.n_ctx - 1));
+            if (it.n_ctx_tiles && lane < 16) {
+                const int vr0 = it.sq.ctx_row0 + min(8 * lane, it.sq.n_ctx - 1);
+                if (a.seq_seg0) cur.start(a, a.seq_seg0[args.work[w].x], vr0);
+                else cur.seek(a, vr0);
+            }
             for (int t = 0; t < it.n_tiles; ++t, ++g) {
                 const int stg = int(g % (is_k ? kKStages : kVStages));
                 const long lap = g / (is_k ? kKStages : kVStages);

@@ -421,6 +421,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
             aa.layer = l;
             aa.layers = c.num_layers;
             aa.kpaged = true;
+            aa.seq_seg0 = a.seq_seg0;
             aa.cos_f = rope_.cos_f();
             aa.sin_f = rope_.sin_f();
         }

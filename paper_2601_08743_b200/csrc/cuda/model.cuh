@@ -88,6 +88,7 @@ struct FwdArgs {
     int gather_n_segs = 0, gather_rows = 0;
     const int4* gather_chunks = nullptr;    // device: {seg, t0, rows, 0} (bf16 fast path)
     size_t gather_pool_bytes = 0;           // pool extent (paged mode's TMA view of the pool)
+    const int32_t* seq_seg0 = nullptr;      // device [n_seqs]: first gather segment of each sequence
     const cudaEvent_t* layer_ready = nullptr;  // optional [L]: layer l's prefix K/V has landed (layer-ordered loads)
     bool paged_v = false, paged_k = false;  // both: the tcgen05 attention reads the prefix from the
                                             // pages (K rotated in smem); else the gather fills the slab

@@ -382,6 +382,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     std::vector<int64_t> pos64;
     std::vector<AttnSeq> seqs;
     std::vector<size_t> seq_query;
+    std::vector<int32_t> seq_seg0;  // per prefilled sequence: its first segment (the attention's page walk)
     int ctx_rows = 0, M = 0;
     size_t group_first = 0;  // first window of the open group
     bool in_dt_set = false;
@@ -555,6 +556,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             R.window_of[qi] = int(wi);
             int cursor = 0;
             const int q_ctx0 = ctx_rows;
+            const int q_seg0 = int(segs.size());
             for (const Seg& s : qsegs[qi - w.begin]) {
                 segs.push_back({int32_t(page_ids.size()), s.tokens, cursor, ctx_rows});
                 page_ids.insert(page_ids.end(), s.pages.begin(), s.pages.end());
@@ -564,6 +566,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             R.total_ctx_tokens += cursor;
             if (q.suffix.empty()) continue;  // nothing to prefill, no first token
             seqs.push_back({M, int(q.suffix.size()), q_ctx0, cursor});
+            seq_seg0.push_back(q_seg0);
             seq_query.push_back(qi);
             for (size_t i = 0; i < q.suffix.size(); ++i) {
                 tokens.push_back(q.suffix[i]);
@@ -630,6 +633,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 fa.gather_pool = pool_.base();
                 fa.gather_page_bytes = P;
                 fa.gather_pool_bytes = P * size_t(pool_.n_pages());
+                fa.seq_seg0 = static_cast<const int32_t*>(ring.upload(seq_seg0.data(), seq_seg0.size() * 4, cs_));
                 fa.gather_pages = d_pages_s;
                 fa.gather_segs = d_segs_s;
                 fa.gather_n_segs = int(segs.size());
@@ -689,7 +693,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
             R.argmax[seq_query[k]] = int32_t(plan.windows[group_first].begin + k);  // slot, resolved below
         dropped.clear();
         segs.clear(), page_ids.clear(), tokens.clear(), pos.clear(), logit_rows.clear(), pos64.clear();
-        seqs.clear(), seq_query.clear();
+        seqs.clear(), seq_query.clear(), seq_seg0.clear();
         ctx_rows = 0, M = 0;
         group_first = wi + 1;
     }
