@@ -480,7 +480,9 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
-    tpath = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2", "roofline_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r1_roofline_traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     achieved_tf = gemm_fl / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
     cpu = None

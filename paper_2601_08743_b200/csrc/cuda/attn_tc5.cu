@@ -223,6 +223,25 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
     return uint64_t((saddr & 0x3FFFF) >> 4) | (uint64_t(kKVHalf >> 4) << 16) | (uint64_t(64) << 32) | (uint64_t(1) << 46) |
            (uint64_t(2) << 61);
 }
+// Paged ctx tiles use a group-interleaved layout: 8-row group g, 64-column half h at g * 2 KB +
+// h * 1 KB (each block one SW128 atom), so one 3-D TMA box {64 cols, 8 rows, 2 halves} fills a whole
+// group. K-major (K tile, B of S = Q.K^T): 8-row groups SBO = 2 KB apart; the second 64 head dims
+// +1 KB. MN-major (V tile, B of O += P.V): the two 64-dim blocks LBO = 1 KB apart, 8-key groups
+// SBO = 2 KB apart.
+constexpr int kGrp = 2048, kGrpHalf = 1024;
+__device__ __forceinline__ uint64_t desc_k_grp(uint32_t saddr) {
+    return uint64_t((saddr & 0x3FFFF) >> 4) | (uint64_t(1) << 16) | (uint64_t(kGrp >> 4) << 32) | (uint64_t(1) << 46) |
+           (uint64_t(2) << 61);
+}
+__device__ __forceinline__ uint64_t desc_mn_grp(uint32_t saddr) {
+    return uint64_t((saddr & 0x3FFFF) >> 4) | (uint64_t(kGrpHalf >> 4) << 16) | (uint64_t(kGrp >> 4) << 32) |
+           (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+// smem byte offset of 16-byte chunk c (0..15) of tile row rr in a grouped paged tile
+__device__ __forceinline__ uint32_t grp_off(int rr, int c) {
+    return uint32_t((rr >> 3) * kGrp + (c >> 3) * kGrpHalf + (rr & 7) * 128 + (((c & 7) ^ (rr & 7)) << 4));
+}
+
 // f16-kind instruction descriptor: D f32, A/B bf16, A K-major, B K- or MN-major, M=128, N=n
 __host__ __device__ constexpr uint32_t idesc(bool b_mn, int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -291,6 +310,11 @@ __device__ __forceinline__ uint32_t gtime() {
         if (args.trace && blockIdx.x == 0 && (idx) < 1024) args.trace[(ev) * 1024 + (idx)] = gtime(); \
     } while (0)
 
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int x, int y, int z, int w) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int x, int y, int z) {
     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
                  "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y), "r"(z)
@@ -300,7 +324,8 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, uint3
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk_ctx,
                     const __grid_constant__ CUtensorMap mv_ctx, const __grid_constant__ CUtensorMap mk_own,
-                    const __grid_constant__ CUtensorMap mv_own, const __grid_constant__ Tc5Args args) {
+                    const __grid_constant__ CUtensorMap mv_own, const __grid_constant__ CUtensorMap mp4,
+                    const __grid_constant__ CUtensorMap mp2, const __grid_constant__ Tc5Args args) {
     const AttnArgs& a = args.a;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -473,10 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!is_k && t * BN + BN > it.sq.n_ctx) {  // V rows past the prefix: finite zeros (P is 0 there)
                     for (int i = lane; i < (t * BN + BN - it.sq.n_ctx) * 16; i += 32) {
                         const int rr = it.sq.n_ctx - t * BN + (i >> 4), c = i & 15;
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst + (c >> 3) * kKVHalf + rr * 128 +
-                                                                             (((c & 7) ^ (rr & 7)) << 4)),
-                                     "r"(0u)
-                                     : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(dst + grp_off(rr, c)), "r"(0u) : "memory");
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
@@ -488,15 +510,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (nv > 0) {
                     const int vr = it.sq.ctx_row0 + key0;
-                    const long pr = cur.pool_row(a, vr, ls);
+                    const uint32_t gdst = dst + lane * kGrp;  // this lane's 8-row group (grouped layout)
+                    long pr = cur.pool_row(a, vr, ls);
+#ifdef TKV_ATTN_FAKE_CLEAN  // timing probe only (wrong rows at boundaries): every full group as one box
+                    if (nv == 8) {
+#else
                     if (nv == 8 && cur.run8(a, vr, ls)) {
-                        for (int h = 0; h < 2; ++h)
-                            tma_2d(dst + h * kKVHalf + 8 * lane * 128, &mk_ctx, fb, it.kvh * D + h * 64, int(pr));
+#endif
+                        tma_4d(gdst, &mk_ctx, fb, 0, int(pr), 0, it.kvh);  // both halves of 8 rows of this head
                     } else {
-                        for (int r = 0; r < nv; ++r) {
-                            const long p1 = r == 0 ? pr : cur.pool_row(a, vr + r, ls);
-                            for (int h = 0; h < 2; ++h)
-                                tma_2d(dst + h * kKVHalf + (8 * lane + r) * 128, &mv_ctx, fb, it.kvh * D + h * 64, int(p1));
+                        // runs of consecutive pool rows inside the group, each as 4 / 2 / 1-row boxes
+                        // per 64-column half (the swizzle follows the smem address, so a box may
+                        // start at any row of the atom)
+                        int r0 = 0;
+                        while (r0 < nv) {
+                            int n = 1;
+                            long pn = pr;
+                            while (r0 + n < nv) {
+                                pn = cur.pool_row(a, vr + r0 + n, ls);
+                                if (pn != pr + n) break;
+                                ++n;
+                            }
+                            for (int r = r0; r < r0 + n;) {
+                                const int len = (r0 + n - r) >= 4 ? 4 : (r0 + n - r) >= 2 ? 2 : 1;
+                                const CUtensorMap* mp = len == 4 ? &mp4 : len == 2 ? &mp2 : &mv_ctx;
+                                for (int h = 0; h < 2; ++h)
+                                    tma_2d(gdst + h * kGrpHalf + r * 128, mp, fb, it.kvh * D + h * 64, int(pr + (r - r0)));
+                                r += len;
+                            }
+                            r0 += n;
+                            pr = pn;  // first row of the next run (when the run broke on pn)
                         }
                     }
                 }
@@ -507,19 +550,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t id_qk = idesc(false, BN), id_pv = idesc(true, D);
             // cursor over the flattened (item, tile) sequence of this CTA
             struct Cur {
-                int w, j, t, n;
+                int w, j, t, n, nct;  // nct: the item's cached-prefix tiles (grouped layout when paged)
                 long gi;
+            };
+            auto set_item = [&](Cur& c) {
+                if (c.w < args.n_work) {
+                    const Item it = item(c.w);
+                    c.n = it.n_tiles, c.nct = it.n_ctx_tiles;
+                } else {
+                    c.n = 0, c.nct = 0;
+                }
             };
             auto first_tile = [&](Cur& c) {
                 c.w = blockIdx.x, c.j = 0, c.t = 0, c.gi = 0;
-                c.n = c.w < args.n_work ? item(c.w).n_tiles : 0;
+                set_item(c);
                 return c.w < args.n_work;
             };
             auto advance = [&](Cur c) {
                 ++c.gi;
                 if (++c.t == c.n) {
                     c.t = 0, c.w += gridDim.x, ++c.j;
-                    c.n = c.w < args.n_work ? item(c.w).n_tiles : 0;
+                    set_item(c);
                 }
                 return c;
             };
@@ -532,9 +583,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c.t == 0) mbar_wait(b_qfull(st), c.j & 1);
                 fence_after();
                 const uint32_t qa = s0 + kQOff + st * kQTile, ka = s0 + kK0 + sk * kKVTile;
+                const bool grp = a.kpaged && c.t < c.nct;  // paged cached-prefix tile: grouped layout
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k)  // K = head dim: A = Q_st, B = K (both K-major)
-                    mma(tmem + st * BN, desc_k(qa + (k >> 2) * kQHalf + (k & 3) * 32), desc_k(ka + (k >> 2) * kKVHalf + (k & 3) * 32),
+                    mma(tmem + st * BN, desc_k(qa + (k >> 2) * kQHalf + (k & 3) * 32),
+                        grp ? desc_k_grp(ka + (k >> 2) * kGrpHalf + (k & 3) * 32) : desc_k(ka + (k >> 2) * kKVHalf + (k & 3) * 32),
                         id_qk, k > 0 ? 1u : 0u);
                 commit(b_sfull(st));
                 if (c.t + 1 == c.n) commit(b_qempty(st));
@@ -551,10 +604,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c.t == 0) mbar_wait(b_ofree(st), (c.j & 1) ^ 1);  // the previous item's epilogue read O_st
                 fence_after();
                 const uint32_t va = s0 + kV0 + sv * kKVTile;
+                const bool grp = a.kpaged && c.t < c.nct;
 #pragma unroll
                 for (int k = 0; k < BN / 16; ++k)  // K = keys: A = P (TMEM, 8 columns per 16 keys), B = V (MN-major)
-                    mma_ts(tmem + 256 + st * D, tmem + st * BN + k * 8, desc_mn(va + k * 16 * 128), id_pv,
-                           (c.t > 0 || k > 0) ? 1u : 0u);
+                    mma_ts(tmem + 256 + st * D, tmem + st * BN + k * 8,
+                           grp ? desc_mn_grp(va + k * 2 * kGrp) : desc_mn(va + k * 16 * 128), id_pv, (c.t > 0 || k > 0) ? 1u : 0u);
                 commit(b_pvdone(st));
                 if (st == 1) commit(b_vempty(sv));
             };
@@ -605,7 +659,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int t = 0; t < it.n_tiles; ++t, ++g) {
                     const int sk = int(g % kKStages);
                     mbar_wait(b_kland(sk), int((g / kKStages) & 1));
+#ifdef TKV_ATTN_NO_ROTATE  // timing probe only: K published unrotated
+                    if (false) {
+#else
                     if (t < it.n_ctx_tiles) {
+#endif
                         const uint32_t dk = s0 + kK0 + sk * kKVTile;
                         const int pos0 = t * BN + 32 * kw + hl;
                         float cs[4], sn[4];
@@ -618,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 4
                         for (int i = 0; i < 16; ++i) {
                             const int rr = 32 * kw + 2 * i + hl;
-                            const uint32_t at = dk + (c >> 3) * kKVHalf + rr * 128 + (((c & 7) ^ (rr & 7)) << 4);
+                            const uint32_t at = dk + grp_off(rr, c);  // grouped paged tile
                             uint32_t wv[4] = {0u, 0u, 0u, 0u};
                             if (pos0 + 2 * i < it.sq.n_ctx) {
                                 asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
@@ -898,6 +956,21 @@ CUtensorMap rows_map(const void* base, long rows, int cols, int box_rows = BN) {
     return m;
 }
 
+// the pool as a 4-D tensor {64 cols, rows, 2 halves (128 B apart), kv heads (256 B apart)}: a
+// {64, 8, 2, 1} box lands as the [half][8 rows][64] pair of SW128 atoms of one group of a grouped
+// paged tile
+CUtensorMap pool_group_map(const void* base, long rows, int kvd) {
+    CUtensorMap m;
+    const cuuint64_t dims[4] = {64, cuuint64_t(std::max(1L, rows)), 2, cuuint64_t(kvd / D)};
+    const cuuint64_t strides[3] = {cuuint64_t(kvd) * 2, 128, 256};
+    const cuuint32_t box[4] = {64, 8, 2, 1}, es[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (pool groups) failed: " + std::to_string(int(r)));
+    return m;
+}
+
 // queries [rows][heads][128] bf16: box = 64 dims x G heads x BM/G tokens, so the tile lands as
 // BM rows (token-major, head-minor) of 128 bytes with the 128-byte swizzle
 CUtensorMap q_map(const void* base, long rows, int heads, int G) {
@@ -927,9 +1000,14 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
     ensure_smem_optin(reinterpret_cast<const void*>(attn_tc5_kernel), kSmem);
     const int kvd = a.kv_heads * D;
     // paged mode: the pool as [pool rows][kv_dim] — 8-row boxes (mkc) and single-row boxes (mvc)
-    const CUtensorMap mkc = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 8)
+    // paged mode: the pool as [pool rows][kv_dim] — one {64 cols, 8 rows, 2 halves} box per 8-row
+    // group (mkc, 3-D view with the halves as a dimension) and 4 / 2 / 1-row boxes of one half for
+    // the runs between table and page boundaries (mp4, mp2, mvc)
+    const CUtensorMap mkc = a.kpaged ? pool_group_map(a.vpool, a.pool_rows, kvd)
                             : a.k_hm_rows ? rows_map(a.k_ctx, a.k_hm_rows * a.kv_heads, D) : rows_map(a.k_ctx, ctx_rows, kvd);
     const CUtensorMap mvc = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 1) : rows_map(a.v_ctx, ctx_rows, kvd);
+    const CUtensorMap mp4 = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 4) : mvc;
+    const CUtensorMap mp2 = a.kpaged ? rows_map(a.vpool, a.pool_rows, kvd, 2) : mvc;
     const CUtensorMap mko = rows_map(a.k_own, own_rows, kvd), mvo = rows_map(a.v_own, own_rows, kvd);
     const CUtensorMap mq = q_map(a.q, own_rows, a.num_heads, a.num_heads / a.kv_heads);
     static const char* trace_path = std::getenv("TKV_ATTN_TRACE");
@@ -940,7 +1018,7 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
     }
     Tc5Args args{a, work, n_work, trace};
     const int n_sm = device_sm_count();
-    attn_tc5_kernel<<<std::min(n_work, n_sm), kThreads, kSmem, s>>>(mq, mkc, mvc, mko, mvo, args);
+    attn_tc5_kernel<<<std::min(n_work, n_sm), kThreads, kSmem, s>>>(mq, mkc, mvc, mko, mvo, mp4, mp2, args);
     TKV_CUDA_CHECK(cudaGetLastError());
     if (trace) {  // debug only: CTA 0's timeline of the latest launch
         std::vector<uint32_t> h(16 * 1024);
