@@ -169,6 +169,16 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -646,12 +656,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int c = lane & 15, hl = lane >> 4;  // chunk of the head row; rows 32 kw + 2i + hl
             constexpr int kRowStep = 2;
             const int half = D / 2;
-            float cd[4], sd[4];  // R(kRowStep theta_k), k = 4c..4c+3
+            // packed f32x2 math: lane q of the pair vectors holds pairs (2q, 2q + 1) of the chunk
+            uint64_t CD[2], SD[2], NSD[2];  // R(kRowStep theta_k), k = 4c..4c+3
             {
                 const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + kRowStep * half + 4 * c));
                 const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + kRowStep * half + 4 * c));
-                cd[0] = x.x, cd[1] = x.y, cd[2] = x.z, cd[3] = x.w;
-                sd[0] = y.x, sd[1] = y.y, sd[2] = y.z, sd[3] = y.w;
+                CD[0] = pack_f32x2(x.x, x.y), CD[1] = pack_f32x2(x.z, x.w);
+                SD[0] = pack_f32x2(y.x, y.y), SD[1] = pack_f32x2(y.z, y.w);
+                NSD[0] = pack_f32x2(-y.x, -y.y), NSD[1] = pack_f32x2(-y.z, -y.w);
             }
             long g = 0;
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x) {
@@ -666,12 +678,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                         const uint32_t dk = s0 + kK0 + sk * kKVTile;
                         const int pos0 = t * BN + 32 * kw + hl;
-                        float cs[4], sn[4];
+                        uint64_t CS[2] = {0ull, 0ull}, SN[2] = {0ull, 0ull};
                         if (pos0 < it.sq.n_ctx) {
                             const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + long(pos0) * half + 4 * c));
                             const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + long(pos0) * half + 4 * c));
-                            cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
-                            sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
+                            CS[0] = pack_f32x2(x.x, x.y), CS[1] = pack_f32x2(x.z, x.w);
+                            SN[0] = pack_f32x2(y.x, y.y), SN[1] = pack_f32x2(y.z, y.w);
                         }
 #pragma unroll 4
                         for (int i = 0; i < 16; ++i) {
@@ -682,24 +694,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                              : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
                                              : "r"(at));
-#ifdef TKV_KROT_TABLE  // A/B knob: cos/sin of every row from the f32 table (bit-exact with the gather)
-                                {
-                                    const long pp = long(pos0 + 2 * i) * half + 4 * c;
-                                    const float4 x = __ldg(reinterpret_cast<const float4*>(a.cos_f + pp));
-                                    const float4 y = __ldg(reinterpret_cast<const float4*>(a.sin_f + pp));
-                                    cs[0] = x.x, cs[1] = x.y, cs[2] = x.z, cs[3] = x.w;
-                                    sn[0] = y.x, sn[1] = y.y, sn[2] = y.z, sn[3] = y.w;
-                                }
-#endif
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    const float x0 = __uint_as_float(wv[j] << 16), x1 = __uint_as_float(wv[j] & 0xffff0000u);
-                                    wv[j] = pack_bf16x2(fmaf(x0, cs[j], -x1 * sn[j]), fmaf(x0, sn[j], x1 * cs[j]));
-#ifndef TKV_KROT_TABLE
-                                    const float cn = fmaf(cs[j], cd[j], -sn[j] * sd[j]);
-                                    sn[j] = fmaf(sn[j], cd[j], cs[j] * sd[j]);
-                                    cs[j] = cn;
-#endif
+                                for (int q = 0; q < 2; ++q) {
+                                    const uint32_t w0 = wv[2 * q], w1 = wv[2 * q + 1];
+                                    const uint64_t X0 = pack_u32x2(w0 << 16, w1 << 16);                  // a of the pairs
+                                    const uint64_t X1 = pack_u32x2(w0 & 0xffff0000u, w1 & 0xffff0000u);  // b
+                                    const uint64_t A = fsub2(fmul2(X0, CS[q]), fmul2(X1, SN[q]));        // a c - b s
+                                    const uint64_t B = ffma2(X0, SN[q], fmul2(X1, CS[q]));              // a s + b c
+                                    float a0, a1, b0, b1;
+                                    unpack_f32x2(A, a0, a1);
+                                    unpack_f32x2(B, b0, b1);
+                                    wv[2 * q] = pack_bf16x2(a0, b0);
+                                    wv[2 * q + 1] = pack_bf16x2(a1, b1);
+                                    const uint64_t cn = ffma2(SN[q], NSD[q], fmul2(CS[q], CD[q]));  // c cd - s sd
+                                    SN[q] = ffma2(CS[q], SD[q], fmul2(SN[q], CD[q]));               // s cd + c sd
+                                    CS[q] = cn;
                                 }
                             }
                             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
