@@ -4,6 +4,7 @@
 //   f32 / f64 (reference-precision path): the SIMT kernels of simt.cu, operation-for-operation
 //     the reference's arithmetic (attention.hpp:210-247 and :368-414).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -16,8 +17,23 @@
 namespace tkv {
 
 // ------------------------------------------------------------------ StagingRing
+// Per-window metadata (tokens, positions, sequences, segments, page ids, tiles) reaches the device
+// through a pinned, device-mapped ring copied by a small SM kernel on the compute stream — NOT by
+// cudaMemcpyAsync: the copy engines are busy with the next window's multi-GB KV page copies, and a
+// DMA upload queued behind them stalled the window's whole prefill until those copies finished
+// (~100 ms per batch at C4: profiles/r2/executor_window_timeline_*).
+namespace {
+__global__ void stage_copy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+    const size_t n16 = n / 16;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += size_t(gridDim.x) * blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    if (blockIdx.x == 0 && threadIdx.x < n % 16) dst[n16 * 16 + threadIdx.x] = src[n16 * 16 + threadIdx.x];
+}
+}  // namespace
+
 StagingRing::StagingRing(size_t bytes) : cap_(bytes) {
-    TKV_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), bytes, cudaHostAllocDefault));
+    TKV_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), bytes, cudaHostAllocMapped));
+    TKV_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_), host_, 0));
     TKV_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&dev_), bytes));
 }
 
@@ -31,7 +47,10 @@ void* StagingRing::upload(const void* src, size_t bytes, cudaStream_t s) {
     reserve(n);
     if (bytes) {
         std::memcpy(host_ + off_, src, bytes);
-        TKV_CUDA_CHECK(cudaMemcpyAsync(dev_ + off_, host_ + off_, bytes, cudaMemcpyHostToDevice, s));
+        const int blocks = int(std::min<size_t>(148, (bytes / 16 + 255) / 256 + 1));
+        stage_copy_kernel<<<blocks, 256, 0, s>>>(dev_ + off_, mapped_ + off_, bytes);
+        TKV_CUDA_CHECK(cudaGetLastError());
+        ++launches_;
     }
     void* d = dev_ + off_;
     off_ += n;
@@ -219,6 +238,18 @@ void Model::add_timed(cudaEvent_t a, cudaEvent_t b, double flops) {
 
 void Model::collect_timing(double& gemm_ms, double& gemm_flops, double& gather_ms, double& attn_ms, double& gather_bytes) {
     gemm_ms = gemm_flops = gather_ms = attn_ms = gather_bytes = 0;
+    static const char* dump = std::getenv("TKV_DUMP_TIMING");  // debug: every timed launch (kind, start, end ms)
+    if (dump && !timed_.empty())
+        if (FILE* f = std::fopen(dump, "a")) {
+            for (const TimedRec& r : timed_) {
+                float a0 = 0, a1 = 0;
+                cudaEventElapsedTime(&a0, timed_.front().a, r.a);
+                cudaEventElapsedTime(&a1, timed_.front().a, r.b);
+                std::fprintf(f, "%d %.4f %.4f %.0f\n", r.kind, a0, a1, r.flops);
+            }
+            std::fprintf(f, "--\n");
+            std::fclose(f);
+        }
     for (const TimedRec& r : timed_) {
         float ms = 0;
         TKV_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));

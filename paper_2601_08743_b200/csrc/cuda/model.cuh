@@ -33,13 +33,17 @@ class StagingRing {
    public:
     explicit StagingRing(size_t bytes);
     ~StagingRing();
-    // copies `n` bytes of `src` into the ring and enqueues the H2D copy on `s`; returns the device pointer
+    // copies `n` bytes of `src` into the ring and enqueues the device-side copy (an SM kernel reading
+    // the mapped ring, so it never queues behind DMA page copies) on `s`; returns the device pointer
     void* upload(const void* src, size_t n, cudaStream_t s);
     // make room for n more bytes without wrapping (wraps, with a device sync, now if needed)
     void reserve(size_t n);
+    long launches() const { return launches_; }  // copy kernels launched so far (gpu_launches claim)
 
    private:
     uint8_t* host_ = nullptr;
+    uint8_t* mapped_ = nullptr;  // device view of host_
+    long launches_ = 0;
     uint8_t* dev_ = nullptr;
     size_t cap_ = 0, off_ = 0;
 };

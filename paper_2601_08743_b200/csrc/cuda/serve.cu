@@ -188,6 +188,7 @@ void Server::ensure_ctx(size_t bytes) {
 ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOptions& opts) {
     ServeResult R;
     if (queries.empty()) return R;
+    const long ring_launches0 = model_.ring().launches();
     const ModelCfg& mc = model_.cfg();
     const int L = mc.num_layers, kvd = mc.kv_dim();
     const DType out_dt = mc.dtype == DType::bf16 ? DType::bf16 : DType::f32;
@@ -739,6 +740,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
     }
     if (opts.time_kernels) model_.collect_timing(R.gemm_ms, R.gemm_flops, R.gather_ms, R.attn_ms, R.gather_bytes);
     if (opts.keep_logits) R.logits = std::move(logits_host);
+    R.launches += model_.ring().launches() - ring_launches0;  // metadata copy kernels
     R.wall_ms = now_ms() - host0;
     if (host_prof)
         std::fprintf(stderr, "[tkv host] tail: sync %.1f ms, results %.1f ms; makespan %.1f, wall %.1f\n", tail1 - tail0,
