@@ -42,19 +42,31 @@ StagingRing::~StagingRing() {
     cudaFree(dev_);
 }
 
+// Uploads are lazy: the bytes land in the pinned ring now and the device pointer is returned at once;
+// flush() copies everything uploaded since the last flush with ONE kernel (the uploads of a window
+// are contiguous in the ring), right before the first kernel that reads them.
 void* StagingRing::upload(const void* src, size_t bytes, cudaStream_t s) {
     const size_t n = (bytes + 255) & ~size_t(255);  // keep every chunk 256-byte aligned
+    if (off_ + n > cap_) flush(s);  // (reserve may wrap: nothing may stay pending across it)
     reserve(n);
     if (bytes) {
         std::memcpy(host_ + off_, src, bytes);
-        const int blocks = int(std::min<size_t>(148, (bytes / 16 + 255) / 256 + 1));
-        stage_copy_kernel<<<blocks, 256, 0, s>>>(dev_ + off_, mapped_ + off_, bytes);
-        TKV_CUDA_CHECK(cudaGetLastError());
-        ++launches_;
+        if (pend_end_ == pend_begin_) pend_begin_ = off_;
+        pend_end_ = off_ + bytes;
     }
     void* d = dev_ + off_;
     off_ += n;
     return d;
+}
+
+void StagingRing::flush(cudaStream_t s) {
+    if (pend_end_ == pend_begin_) return;
+    const size_t bytes = pend_end_ - pend_begin_;
+    const int blocks = int(std::min<size_t>(148, (bytes / 16 + 255) / 256 + 1));
+    stage_copy_kernel<<<blocks, 256, 0, s>>>(dev_ + pend_begin_, mapped_ + pend_begin_, bytes);
+    TKV_CUDA_CHECK(cudaGetLastError());
+    ++launches_;
+    pend_begin_ = pend_end_ = 0;
 }
 
 void StagingRing::reserve(size_t n) {
@@ -217,10 +229,12 @@ void Model::ensure_ws(int M, cudaStream_t s) {
 void Model::forward(const FwdArgs& a, cudaStream_t s) {
     if (a.M == 0) return;
     ensure_ws(a.M, s);
-    if (cfg_.dtype == DType::bf16)
-        forward_bf16(a, s);
-    else
+    if (cfg_.dtype == DType::bf16) {
+        forward_bf16(a, s);  // flushes the staging ring after its own uploads
+    } else {
+        ring_.flush(s);
         forward_ref(a, s);
+    }
 }
 
 cudaEvent_t Model::timing_event() {
@@ -372,6 +386,7 @@ void Model::forward_bf16(const FwdArgs& a, cudaStream_t s) {
         }
     };
 
+    ring_.flush(s);  // every metadata upload of this forward (and the caller's) reaches HBM here
     embed_norm_bf16(emb_, a.tokens, M, h, x, xn, rms, eps, s);
     ++nl;
     for (int l = 0; l < c.num_layers; ++l) {

@@ -33,9 +33,11 @@ class StagingRing {
    public:
     explicit StagingRing(size_t bytes);
     ~StagingRing();
-    // copies `n` bytes of `src` into the ring and enqueues the device-side copy (an SM kernel reading
-    // the mapped ring, so it never queues behind DMA page copies) on `s`; returns the device pointer
+    // copies `n` bytes of `src` into the ring and returns the device pointer; the device-side copy (an
+    // SM kernel reading the mapped ring, so it never queues behind DMA page copies) runs at flush()
     void* upload(const void* src, size_t n, cudaStream_t s);
+    // copy every upload since the last flush to HBM (one kernel on `s`): call before a kernel reads them
+    void flush(cudaStream_t s);
     // make room for n more bytes without wrapping (wraps, with a device sync, now if needed)
     void reserve(size_t n);
     long launches() const { return launches_; }  // copy kernels launched so far (gpu_launches claim)
@@ -44,6 +46,7 @@ class StagingRing {
     uint8_t* host_ = nullptr;
     uint8_t* mapped_ = nullptr;  // device view of host_
     long launches_ = 0;
+    size_t pend_begin_ = 0, pend_end_ = 0;  // ring bytes uploaded but not yet copied
     uint8_t* dev_ = nullptr;
     size_t cap_ = 0, off_ = 0;
 };
@@ -187,6 +190,7 @@ class Model {
     int ws_rows_ = 0;
     void* ws_ = nullptr;
     long launches_ = 0;
+    size_t pend_begin_ = 0, pend_end_ = 0;  // ring bytes uploaded but not yet copied
 };
 
 }  // namespace tkv

@@ -608,6 +608,7 @@ ServeResult Server::serve(const std::vector<ServeQuery>& queries, const ServeOpt
                 g1 = evp.get();
                 TKV_CUDA_CHECK(cudaEventRecord(g0, cs_));
             }
+            ring.flush(cs_);
             launch_gather_rope(pool_.base(), P, d_pages, d_segs, int(segs.size()), ctx_rows, L, kvd, mc.head_dim, in_dt,
                                out_dt, model_.rope().cos_d(), model_.rope().sin_d(), model_.rope().cos_f(),
                                model_.rope().sin_f(), ctx_k, ctx_v, max_ctx_rows, cs_);
