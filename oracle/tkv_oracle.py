@@ -825,10 +825,21 @@ def attend(q, k, v, cfg, allow):
     return out
 
 
+def _norm_in(x, cfg, storage, first_layer):
+    """The projection input norm(x). The bf16 mirror follows the CUDA path's RMSNorm fold
+    (gemm_tc.cuh EpiParams, model.cu forward_bf16): for RMS models with hidden % 512 == 0 every
+    projection after the embedding's reads bf16(x) and scales its accumulator rows by
+    rsqrt(mean(x^2) + eps) of the f32 residual, i.e. norm(x) is bf16(x) * r, not bf16(x * r)."""
+    if storage == "bf16" and cfg.norm == "rms" and cfg.hidden % 512 == 0 and not first_layer:
+        r = 1.0 / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + cfg.eps)
+        return round_bf16(x) * r
+    return storage_round(storage)(norm_rows(x, cfg))
+
+
 def _ffn(x, L, cfg, storage):
     """attention.hpp:192-203 (LN -> W_in -> SiLU -> W_out -> residual), + SwiGLU extension."""
     rnd = storage_round(storage)
-    xn = rnd(norm_rows(x, cfg))
+    xn = _norm_in(x, cfg, storage, False)
     up = xn @ L["ffn_in"].T
     if _ref_storage(storage):
         up = rnd(up)
@@ -853,7 +864,7 @@ def forward(cfg, W: Weights, own_tokens, own_pos, ctx_k=None, ctx_v=None, allow=
     n_ctx = 0 if ctx_k is None else ctx_k[0].shape[0]
     k_raw_l, k_rot_l, v_l = [], [], []
     for l, L in enumerate(W.layers):
-        xn = rnd(norm_rows(x, cfg))
+        xn = _norm_in(x, cfg, storage, l == 0)
         q = xn @ L["wq"].T
         k = xn @ L["wk"].T
         v = rnd(xn @ L["wv"].T)
