@@ -64,6 +64,12 @@ constexpr int kStreamBars = 4;
 constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars + kKStages;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
 static_assert(kSmem <= 227 * 1024, "attention smem over the per-CTA limit");
+#ifndef TKV_ATTN_SINGLE_STREAM
+#define TKV_ATTN_SINGLE_STREAM 1
+#endif
+// an item whose tokens all fit the first Q tile runs stream 0 alone (no Q1 load, QK1 / PV1 or
+// stream-1 softmax); 0 keeps both streams on every item (A/B)
+constexpr bool kSingleStreamItems = TKV_ATTN_SINGLE_STREAM != 0;
 // TMEM columns: S_s (f32, P_s as packed bf16 over its first 64 columns) at 128 s, O_s at 256 + 128 s
 constexpr int kTmemCols = 512;
 
@@ -310,6 +316,7 @@ struct Tc5Args {
     uint32_t* trace;   // debug timeline of CTA 0 (TKV_ATTN_TRACE), else null
 };
 
+constexpr int kTraceEvents = 24;  // TKV_ATTN_TRACE rows of 1024 timestamps (attn_trace.py)
 __device__ __forceinline__ uint32_t gtime() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -392,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     struct Item {
         AttnSeq sq;
         int tok0, kvh, n_tok, n_ctx_tiles, n_tiles;
+        bool two;  // stream 1 has live rows (else the item is single-stream: no Q1, no QK1 / PV1, no softmax 1)
     };
     auto item = [&](int w) {
         const int4 wi = args.work[w];
@@ -402,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it.n_tok = min(2 * TQ, it.sq.n_own - it.tok0);
         it.n_ctx_tiles = (it.sq.n_ctx + BN - 1) / BN;
         it.n_tiles = it.n_ctx_tiles + (it.tok0 + it.n_tok + BN - 1) / BN;  // own keys up to the item's causal bound
+        it.two = it.n_tok > TQ || !kSingleStreamItems;
         return it;
     };
     auto tile_row = [&](const Item& it, int t, bool& ctx) {
@@ -415,16 +424,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA: the item's two Q tiles, then its K tiles
             long g = 0;
-            int j = 0;
+            int j = 0, j1 = 0;  // items so far; items with stream 1 so far
             for (int w = blockIdx.x; w < args.n_work; w += gridDim.x, ++j) {
                 const Item it = item(w);
-                for (int st = 0; st < 2; ++st) {
-                    mbar_wait(b_qempty(st), (j & 1) ^ 1);
+                for (int st = 0; st < (it.two ? 2 : 1); ++st) {
+                    mbar_wait(b_qempty(st), ((st ? j1 : j) & 1) ^ 1);
                     mbar_expect_tx(b_qfull(st), kQTile);
                     for (int h = 0; h < 2; ++h)
                         tma_3d(s0 + kQOff + st * kQTile + h * kQHalf, &mq, b_qfull(st), h * 64, it.kvh * G,
                                it.sq.q_row0 + it.tok0 + st * TQ);
                 }
+                j1 += it.two;
                 TR(8, j);
                 if (a.kpaged) continue;  // paged mode: K tiles come from the K issuer warp
                 auto prefetch_kv = [&](int t) {  // K always; V here only when it comes by TMA
@@ -559,27 +569,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ---- MMA issuer
             const uint32_t id_qk = idesc(false, BN), id_pv = idesc(true, D);
             // cursor over the flattened (item, tile) sequence of this CTA
+            // stream 1's barriers run on their own counters (j1: items with stream 1 before this
+            // one, g1: stream-1 tiles before this one) because single-stream items skip them
             struct Cur {
-                int w, j, t, n, nct;  // nct: the item's cached-prefix tiles (grouped layout when paged)
-                long gi;
+                int w, j, j1, t, n, nct;  // nct: the item's cached-prefix tiles (grouped layout when paged)
+                long gi, g1;
+                bool two;
             };
             auto set_item = [&](Cur& c) {
                 if (c.w < args.n_work) {
                     const Item it = item(c.w);
-                    c.n = it.n_tiles, c.nct = it.n_ctx_tiles;
+                    c.n = it.n_tiles, c.nct = it.n_ctx_tiles, c.two = it.two;
                 } else {
-                    c.n = 0, c.nct = 0;
+                    c.n = 0, c.nct = 0, c.two = false;
                 }
             };
             auto first_tile = [&](Cur& c) {
-                c.w = blockIdx.x, c.j = 0, c.t = 0, c.gi = 0;
+                c.w = blockIdx.x, c.j = 0, c.j1 = 0, c.t = 0, c.gi = 0, c.g1 = 0;
                 set_item(c);
                 return c.w < args.n_work;
             };
             auto advance = [&](Cur c) {
                 ++c.gi;
+                c.g1 += c.two;
                 if (++c.t == c.n) {
                     c.t = 0, c.w += gridDim.x, ++c.j;
+                    c.j1 += c.two;
                     set_item(c);
                 }
                 return c;
@@ -590,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(b_kfull(sk), int((c.gi / kKStages) & 1));
                     TR(2, c.gi);
                 }
-                if (c.t == 0) mbar_wait(b_qfull(st), c.j & 1);
+                if (c.t == 0) mbar_wait(b_qfull(st), (st ? c.j1 : c.j) & 1);
                 fence_after();
                 const uint32_t qa = s0 + kQOff + st * kQTile, ka = s0 + kK0 + sk * kKVTile;
                 const bool grp = a.kpaged && c.t < c.nct;  // paged cached-prefix tile: grouped layout
@@ -600,8 +615,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         grp ? desc_k_grp(ka + (k >> 2) * kGrpHalf + (k & 3) * 32) : desc_k(ka + (k >> 2) * kKVHalf + (k & 3) * 32),
                         id_qk, k > 0 ? 1u : 0u);
                 commit(b_sfull(st));
+                if (st == 0) TR(19, c.gi);
                 if (c.t + 1 == c.n) commit(b_qempty(st));
-                if (st == 1) commit(b_kempty(sk));
+                if (st == 1 || !c.two) commit(b_kempty(sk));
             };
             auto pv = [&](const Cur& c, int st) {  // O_st += P_st . V(c), P_st from TMEM
                 const int sv = int(c.gi % kVStages);
@@ -609,9 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
                     TR(11, c.gi);
                 }
-                mbar_wait(b_pfull(st), int(c.gi & 1));
-                if (st == 0) TR(4, c.gi);
-                if (c.t == 0) mbar_wait(b_ofree(st), (c.j & 1) ^ 1);  // the previous item's epilogue read O_st
+                mbar_wait(b_pfull(st), int((st ? c.g1 : c.gi) & 1));
+                TR(st == 0 ? 4 : 18, c.gi);
+                if (c.t == 0) mbar_wait(b_ofree(st), ((st ? c.j1 : c.j) & 1) ^ 1);  // the previous item's epilogue read O_st
                 fence_after();
                 const uint32_t va = s0 + kV0 + sv * kKVTile;
                 const bool grp = a.kpaged && c.t < c.nct;
@@ -620,21 +636,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ts(tmem + 256 + st * D, tmem + st * BN + k * 8,
                            grp ? desc_mn_grp(va + k * 2 * kGrp) : desc_mn(va + k * 16 * 128), id_pv, (c.t > 0 || k > 0) ? 1u : 0u);
                 commit(b_pvdone(st));
-                if (st == 1) commit(b_vempty(sv));
+                if (st == 1 || !c.two) commit(b_vempty(sv));
+                TR(16 + st, c.gi);
             };
             Cur cur;
             if (first_tile(cur)) {
                 qk(cur, 0);
-                qk(cur, 1);
+                if (cur.two) qk(cur, 1);
                 while (true) {
                     const Cur nxt = advance(cur);
                     const bool more = nxt.w < args.n_work;
                     // PV_s(t) then QK_s(t+1): the tensor pipe executes in issue order, so QK_s(t+1)
-                    // overwrites S_s / P_s only after PV_s(t) has consumed P_s
+                    // overwrites S_s / P_s only after PV_s(t) — or stream s's last PV of an earlier
+                    // item — has consumed P_s
                     pv(cur, 0);
                     if (more) qk(nxt, 0);
-                    pv(cur, 1);
-                    if (more) qk(nxt, 1);
+                    if (cur.two) pv(cur, 1);
+                    if (more && nxt.two) qk(nxt, 1);
                     TR(3, cur.gi);
                     if (!more) break;
                     cur = nxt;
@@ -735,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int j = 0;
         for (int w = blockIdx.x; w < args.n_work; w += gridDim.x, ++j) {
             const Item it = item(w);
+            if (st == 1 && !it.two) continue;  // single-stream item: stream 1's counters do not move
             const AttnSeq& sq = it.sq;
             const int tok_local = st * TQ + r / G;  // token within the item
             const bool live = tok_local < it.n_tok;
@@ -755,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int seg_end = ctx ? sq.n_ctx : sq.n_ctx + sq.n_own;
                 mbar_wait(b_sfull(st), int(gi & 1));
                 if (warp == 4 && lane == 0) TR(5, gi);
+                if (warp == 8 && lane == 0) TR(20, gi);  // stream 1's S ready
                 if (wdead) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(b_pfull(st));
@@ -863,8 +883,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else
 #endif
                         {
+#ifdef TKV_ATTN_NO_EXP_PROBE  // timing probe only (wrong P): the exponentials skipped
+                            p0 = a0;
+                            p1 = a1;
+#else
                             p0 = ex2(a0);
                             p1 = ex2(a1);
+#endif
                         }
 #ifdef TKV_ATTN_PTRUNC  // measured slower (DESIGN §8 "Measured and not kept"); kept as a build knob
                         // bf16 P by truncation (one PRMT per pair on the ALU instead of an F2FP), and
@@ -890,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 unpack_f32x2(acc[1], s2, s3);
                 l_run += (s0 + s1) + (s2 + s3);
                 if (warp == 4 && lane == 0) TR(14, gi);
+                if (warp == 8 && lane == 0) TR(21, gi);  // stream 1's exponentials done
                 if (any_grow) {
                     mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
                     fence_after();
@@ -1022,15 +1048,15 @@ void attention_tc5(const AttnArgs& a, const int4* work, int n_work, long ctx_row
     static const char* trace_path = std::getenv("TKV_ATTN_TRACE");
     uint32_t* trace = nullptr;
     if (trace_path) {
-        TKV_CUDA_CHECK(cudaMalloc(&trace, 16 * 1024 * 4));
-        TKV_CUDA_CHECK(cudaMemsetAsync(trace, 0, 16 * 1024 * 4, s));
+        TKV_CUDA_CHECK(cudaMalloc(&trace, kTraceEvents * 1024 * 4));
+        TKV_CUDA_CHECK(cudaMemsetAsync(trace, 0, kTraceEvents * 1024 * 4, s));
     }
     Tc5Args args{a, work, n_work, trace};
     const int n_sm = device_sm_count();
     attn_tc5_kernel<<<std::min(n_work, n_sm), kThreads, kSmem, s>>>(mq, mkc, mvc, mko, mvo, mp4, mp2, args);
     TKV_CUDA_CHECK(cudaGetLastError());
     if (trace) {  // debug only: CTA 0's timeline of the latest launch
-        std::vector<uint32_t> h(16 * 1024);
+        std::vector<uint32_t> h(kTraceEvents * 1024);
         TKV_CUDA_CHECK(cudaStreamSynchronize(s));
         TKV_CUDA_CHECK(cudaMemcpy(h.data(), trace, h.size() * 4, cudaMemcpyDeviceToHost));
         cudaFree(trace);
