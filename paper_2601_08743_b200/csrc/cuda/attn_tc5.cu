@@ -6,7 +6,8 @@
 // two Q tiles share every 128-key K/V tile and run as two softmax streams that ping-pong on the
 // tensor core (the FlashAttention-4 structure). Persistent: one CTA per SM walks the items
 // (heaviest first); every role keeps a running tile counter, so rings and mbarrier phases run on
-// from one item into the next.
+// from one item into the next. An item whose tokens all fit the first Q tile is single-stream:
+// stream 1 sits it out, so stream 1's barriers count their own items / tiles (j1, g1).
 // Warp 0: TMA lanes (lane 0: the item's two Q tiles + K tiles, lane 16: V tiles; 2-deep rings of
 // 32 KB tiles) from the prefix slab or the own-row buffer (a tile never straddles the two).
 // Paged prefix (the serving path): cached-prefix tiles come straight from the tables' pool pages,
