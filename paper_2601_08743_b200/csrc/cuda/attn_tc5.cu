@@ -61,7 +61,13 @@ constexpr int kQOff = 0, kK0 = 2 * kQTile, kV0 = kK0 + kKStages * kKVTile;
 constexpr int kBarOff = kV0 + kVStages * kKVTile;
 // QFULL[2] QEMPTY[2] KFULL[K] KEMPTY[K] VFULL[V] VEMPTY[V], per stream: SFULL PFULL PVDONE OFREE,
 // then KLAND[K] (paged: raw K rows landed, before the in-place rotation publishes KFULL)
-constexpr int kStreamBars = 4;
+#ifndef TKV_ATTN_PHALF
+#define TKV_ATTN_PHALF 0
+#endif
+// TKV_ATTN_PHALF=1: P is published in two halves (keys 0-63, then 64-127) so PV's first four
+// k-steps run while the softmax computes the second half (adds a per-stream PHALF barrier)
+constexpr bool kPHalf = TKV_ATTN_PHALF != 0;
+constexpr int kStreamBars = kPHalf ? 5 : 4;
 constexpr int kNumBars = 4 + 2 * kKStages + 2 * kVStages + 2 * kStreamBars + kKStages;
 constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;
 static_assert(kSmem <= 227 * 1024, "attention smem over the per-CTA limit");
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto b_pvdone = [&](int st) { return bar(kSB + st * kStreamBars + 2); };
     auto b_ofree = [&](int st) { return bar(kSB + st * kStreamBars + 3); };
     auto b_kland = [&](int i) { return bar(kSB + 2 * kStreamBars + i); };
+    auto b_phalf = [&](int st) { return bar(kSB + st * kStreamBars + 4); };  // kPHalf only
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kBarOff + kNumBars * 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -376,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_qempty(st), 1);
             mbar_init(b_sfull(st), 1);
             mbar_init(b_pfull(st), 4);
+            if (kPHalf) mbar_init(b_phalf(st), 4);
             mbar_init(b_pvdone(st), 1);
             mbar_init(b_ofree(st), 4);
         }
@@ -626,16 +634,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(b_vfull(sv), int((c.gi / kVStages) & 1));
                     TR(11, c.gi);
                 }
-                mbar_wait(b_pfull(st), int((st ? c.g1 : c.gi) & 1));
+                const int pph = int((st ? c.g1 : c.gi) & 1);
+                mbar_wait(kPHalf ? b_phalf(st) : b_pfull(st), pph);
                 TR(st == 0 ? 4 : 18, c.gi);
                 if (c.t == 0) mbar_wait(b_ofree(st), ((st ? c.j1 : c.j) & 1) ^ 1);  // the previous item's epilogue read O_st
                 fence_after();
                 const uint32_t va = s0 + kV0 + sv * kKVTile;
                 const bool grp = a.kpaged && c.t < c.nct;
 #pragma unroll
-                for (int k = 0; k < BN / 16; ++k)  // K = keys: A = P (TMEM, 8 columns per 16 keys), B = V (MN-major)
+                for (int k = 0; k < BN / 16; ++k) {  // K = keys: A = P (TMEM, 8 columns per 16 keys), B = V (MN-major)
+                    if (kPHalf && k == BN / 32) {  // keys 64-127: the second half of P
+                        mbar_wait(b_pfull(st), pph);
+                        fence_after();
+                    }
                     mma_ts(tmem + 256 + st * D, tmem + st * BN + k * 8,
                            grp ? desc_mn_grp(va + k * 2 * kGrp) : desc_mn(va + k * 16 * 128), id_pv, (c.t > 0 || k > 0) ? 1u : 0u);
+                }
                 commit(b_pvdone(st));
                 if (st == 1 || !c.two) commit(b_vempty(sv));
                 TR(16 + st, c.gi);
@@ -778,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (warp == 8 && lane == 0) TR(20, gi);  // stream 1's S ready
                 if (wdead) {
                     __syncwarp();
+                    if (lane == 0 && kPHalf) mbar_arrive(b_phalf(st));
                     if (lane == 0) mbar_arrive(b_pfull(st));
                     continue;
                 }
@@ -856,6 +871,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // lands on columns [16k, 16k+16), all of which pass 2 has already read)
                 const uint64_t sl2x2 = pack_f32x2(sl2, sl2), nbx2 = pack_f32x2(nb, nb);
                 uint64_t acc[2] = {0ull, 0ull};
+                auto rescale_o = [&]() {
+                    mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
+                    fence_after();
+#pragma unroll
+                    for (int c = 0; c < D; c += 32) {
+                        float o[32];
+                        tmem_ld32(tO + c, o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] *= corr;
+                        tmem_st32(tO + c, o);
+                    }
+                };
 #ifdef TKV_ATTN_TWOPASS
                 tmem_ld32_async(tS, ua);
                 tmem_wait_ld();
@@ -904,6 +931,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     }
                     tmem_st16(tS + 16 * k, pk);
+                    if (kPHalf && k == 1) {  // keys 0-63 of P (and O rescaled) before PV's first half
+                        if (any_grow) rescale_o();
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(b_phalf(st));
+                    }
 #ifdef TKV_ATTN_TWOPASS
                     if (k < 3) {
                         tmem_wait_ld();
@@ -917,18 +951,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l_run += (s0 + s1) + (s2 + s3);
                 if (warp == 4 && lane == 0) TR(14, gi);
                 if (warp == 8 && lane == 0) TR(21, gi);  // stream 1's exponentials done
-                if (any_grow) {
-                    mbar_wait(b_pvdone(st), int((gi - 1) & 1));  // O is stable after P(t-1).V
-                    fence_after();
-#pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        float o[32];
-                        tmem_ld32(tO + c, o);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] *= corr;
-                        tmem_st32(tO + c, o);
-                    }
-                }
+                if (!kPHalf && any_grow) rescale_o();
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
                 __syncwarp();

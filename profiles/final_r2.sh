@@ -1,4 +1,4 @@
-# End-of-round-2 evidence run on one B200: full GPU suite (+ the Llama-width parity report), smoke,
+# End-of-round-2 evidence run (re-run after the single-stream attention items) on one B200: full GPU suite (+ the Llama-width parity report), smoke,
 # the default C4 line and the other configurations, the reference CPU arm, the 2-rank path on one
 # GPU, the launch list of one C4 serving step and a --set full capture of its GEMMs (roofline traffic).
 set -u
