@@ -101,19 +101,31 @@ void gather_f32(const ModelConfig& cfg, const std::vector<const TableKV<float>*>
     if (total == 0) return;
     Slot& s = model_for(cfg, 0);
     std::lock_guard<std::mutex> use(s.mu);  // the gather only uses the model's rope tables (seed-free)
-    tkv::Arena arena;
+    // Table images live in pageable host buffers for the length of this call (copy-engine DMA from
+    // pageable memory): a pinned Arena here would pin a 256 MiB chunk per assemble() call, which
+    // dominated the reference acceptance gate's 100-corpus criterion.
     tkv::PagePool pool(P, int(pages));
     std::vector<tkv::GatherSeg> segs;
     std::vector<int32_t> page_ids;
-    std::vector<float> image;
+    std::vector<std::vector<float>> images(tables.size());
     int cursor = 0;
     for (size_t i = 0; i < tables.size(); ++i) {
         const auto* t = tables[i];
         if (t->token_count == 0) continue;
-        image.clear();  // the .kv payload layout: K layers then V layers
+        auto& image = images[i];  // the .kv payload layout: K layers then V layers
         for (const auto& l : t->k) image.insert(image.end(), l.begin(), l.end());
         for (const auto& l : t->v) image.insert(image.end(), l.begin(), l.end());
-        const auto& img = arena.put(int(i), t->token_count, L, kvd, t->local_offset, tkv::DType::f32, image.data());
+        tkv::TableImage img;
+        img.table_id = int(i);
+        img.tokens = t->token_count;
+        img.layers = L;
+        img.kv_dim = kvd;
+        img.local_offset = t->local_offset;
+        img.dtype = tkv::DType::f32;
+        img.bytes = image.size() * sizeof(float);
+        img.host = reinterpret_cast<uint8_t*>(image.data());
+        if (img.bytes != size_t(2) * L * t->token_count * kvd * sizeof(float))
+            throw Error(Errc::dimension_mismatch, "KV block shape does not match model config");
         auto pg = pool.alloc(int((img.bytes + P - 1) / P));
         tkv::copy_table_to_pages(img, pool, pg, tkv::CopyEngine::dma, 16, s.stream);
         segs.push_back({int32_t(page_ids.size()), t->token_count, cursor, cursor});
