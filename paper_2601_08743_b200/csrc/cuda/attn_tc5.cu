@@ -77,6 +77,10 @@ static_assert(kSmem <= 227 * 1024, "attention smem over the per-CTA limit");
 // an item whose tokens all fit the first Q tile runs stream 0 alone (no Q1 load, QK1 / PV1 or
 // stream-1 softmax); 0 keeps both streams on every item (A/B)
 constexpr bool kSingleStreamItems = TKV_ATTN_SINGLE_STREAM != 0;
+#ifndef TKV_ATTN_Q_PREFETCH
+#define TKV_ATTN_Q_PREFETCH 1
+#endif
+constexpr bool kQPrefetch = TKV_ATTN_Q_PREFETCH != 0;  // L2 prefetch of the next item's Q tiles (0: A/B)
 // TMEM columns: S_s (f32, P_s as packed bf16 over its first 64 columns) at 128 s, O_s at 256 + 128 s
 constexpr int kTmemCols = 512;
 
@@ -107,6 +111,11 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint3
 // under load (several us with K and V streaming on every SM) is hidden by pulling it into L2 early
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int x, int y) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(m)), "r"(x),
+                 "r"(y), "r"(z)
                  : "memory");
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -445,6 +454,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 j1 += it.two;
                 TR(8, j);
+                // the next item's Q tiles into L2 now: their TMA load can only issue once this item's
+                // last QK has read the Q buffers, and a cold load then sits on the item boundary
+                // (several us under the K/V streams — most of a short item's time at C2)
+                if (kQPrefetch && w + int(gridDim.x) < args.n_work) {
+                    const Item nx = item(w + gridDim.x);
+                    for (int st = 0; st < (nx.two ? 2 : 1); ++st)
+                        for (int h = 0; h < 2; ++h) tma_prefetch_3d(&mq, h * 64, nx.kvh * G, nx.sq.q_row0 + nx.tok0 + st * TQ);
+                }
                 if (a.kpaged) continue;  // paged mode: K tiles come from the K issuer warp
                 auto prefetch_kv = [&](int t) {  // K always; V here only when it comes by TMA
                     bool ctx;
